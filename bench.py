@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the Bi-cADMM hot path on B200 (one JSON line on rank 0).
+
+Metric (BASELINE.json): Bi-cADMM inner iterations/s (+ GEMV HBM GB/s vs peak).
+Unit: node-level inner iterations per second -- one Algorithm-2 sharing-ADMM
+sweep (Eqs. (22)-(24): GEMV-T, H-apply, GEMV, block sum, prox, dual update) of
+one node's local problem, summed over all nodes of the job.
+
+Workload (N=1): configs[1], sparse logistic regression, 4 nodes x m_i = 25,000
+samples (m = 100k), n = 10,000 features, kappa = 100, one feature block per node
+(M = 1), FP64.  A "step" is one outer Bi-cADMM iteration: K_in = 10 inner sweeps
+on every node, then the global step (Collect, (7b), (13), (14), (9), (15)) and
+the per-iteration residual read-back.  Inputs (8 GB of A) exceed the 126 MB L2,
+so no flush is needed between steps.
+
+Multi-GPU (torchrun, N > 1): weak scaling -- every rank holds 4 more nodes of the
+same shape (node-major placement: no per-sweep exchange); the consensus step
+all-reduces the n-vector sum_i (x_i + u_i) and the node residuals over NCCL.
+
+--impl reference: the FP64 CPU oracle (oracle/, test infrastructure) timed as it
+stands on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Bi-cADMM inner iters/sec and time-to-tol at 1/2/4/8 B200; GEMV HBM GB/s vs peak"
+UNIT = "inner_iters/s"
+WORKLOAD = ("configs[1]: sparse logistic regression, N=4 nodes x m_i=25000 (m=100k), n=10000, kappa=100, "
+            "M=1 feature block per node, FP64, K_in=10 inner sweeps per outer step")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--inner", type=int, default=10)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--nodes", type=int, default=4, help="nodes per rank")
+    ap.add_argument("--m", type=int, default=25_000)
+    ap.add_argument("--n", type=int, default=10_000)
+    ap.add_argument("--kappa", type=int, default=100)
+    ap.add_argument("--loss", default="logistic")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-m", type=int, default=25_000, help="cpu_baseline sample rows")
+    ap.add_argument("--cpu-n", type=int, default=1_000, help="cpu_baseline sample columns")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        self.dev = device_index
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except Exception:
+                continue
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_sample(m: int, n_s: int, inner: int, steps: int, warmup: int, n_full: int, m_full: int, seed=7):
+    """Time the oracle's node-level inner sweeps on a bounded sample (1 node, m rows x
+    n_s columns of the same distribution); returns node-sweeps/s scaled by the
+    per-sweep algorithmic-byte ratio to the full (m_full x n_full) node."""
+    from oracle import oracle as orc
+    from paper_2405_16267_b200 import datagen as dg
+    import numpy as np
+    P = dg.generate(1, m, n_s, max(1, n_s // 100), "logistic", seed=seed)
+    pb = orc.Problem([P.A[0].numpy()], [P.b[0].numpy()], orc.LOGISTIC, 1, np.array([0, n_s]))
+    total = warmup + steps
+    r = orc.run(pb, orc.Params(kappa=max(1, n_s // 100), max_outer=total, inner_fixed=inner, refit=0,
+                               eps_p=0, eps_d=0, eps_b=0))
+    # setup (Gram + Cholesky) is not part of a sweep; inner_s covers every outer step
+    sweeps = total * inner
+    per_sweep_s = r["timings"]["inner_s"] / sweeps
+    bytes_sample = 8 * (2 * m * n_s + n_s * n_s)
+    bytes_full = 8 * (2 * m_full * n_full + n_full * n_full)
+    scale = bytes_full / bytes_sample
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return dict(node_sweeps_per_s_sample=1.0 / per_sweep_s, scale=scale,
+                value=1.0 / per_sweep_s / scale, cores=cores, setup_s=r["timings"]["setup_s"],
+                sample=f"oracle: 1 node, m_i={m} x n={n_s} (same distribution), {sweeps} inner sweeps "
+                       f"({total} outer steps x K_in={inner}); per-sweep time scaled by the algorithmic-byte "
+                       f"ratio {scale:.2f} to a full m_i={m_full} x n={n_full} node")
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2405_16267_b200 import bicadmm as bc
+    from paper_2405_16267_b200 import datagen as dg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = torch.float64 if args.dtype == "f64" else torch.float32
+    nl = args.nodes
+    N = nl * world
+    n, m = args.n, args.m
+    cs = dg.block_partition(n, 1)
+    P = dg.generate(nl, m, n, args.kappa, args.loss, seed=1000 + rank, device="cuda", dtype=dtype)
+    comm = None
+    if world > 1:
+        uid = [bc.bicadmm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = bc.bicadmm_comm_init(world, rank, local, uid[0], rank)  # node-major: own group
+    b_all = [None] * N
+    blocks = []
+    for k in range(nl):
+        i = rank * nl + k
+        b_all[i] = P.b[k]
+        blocks.append((i, 0, P.A[k]))
+    prm = bc.Params(kappa=args.kappa, max_outer=10 ** 6, inner_fixed=args.inner, refit=0,
+                    eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    t0 = time.time()
+    solver = bc.BiCADMM(None, b_all, args.loss, prm, cs, blocks=blocks, comm=comm)
+    setup_wall = time.time() - t0
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        solver.iterate(1)
+    solver.set_profiling(True)
+    launches0 = solver.launches()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        solver.iterate(1)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = solver.launches() - launches0
+    phases = solver.phases()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sweeps = args.steps * args.inner
+    value = N * sweeps / (ms / 1e3)
+    sc = solver.scalars()
+
+    # roofline of the dominant kernel (an HBM pass over every local A_ij)
+    s = 8 if args.dtype == "f64" else 4
+    A_bytes = nl * m * n * s
+    byt = {"gemv": A_bytes + nl * (8 * n + 8 * m), "gemv_t_partial": A_bytes + nl * 16 * m,
+           "h_apply": nl * (n * n * s + 16 * n)}
+    cand = {k: phases[k] for k in byt if phases[k][1] > 0}
+    dom = max(cand, key=lambda k: cand[k][0])
+    dms, dcnt = cand[dom]
+    avg_s = dms / dcnt / 1e3
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = byt[dom] / avg_s / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(dom, {}).get("bytes_per_launch")
+    except Exception:
+        pass
+    total_phase = sum(v[0] for v in phases.values())
+    kernels = {k: {"ms_per_launch": (v[0] / v[1] if v[1] else None), "launches": v[1],
+                   "share": v[0] / total_phase if total_phase else None,
+                   **({"GB_per_s": byt[k] / (v[0] / v[1] / 1e3) / 1e9} if k in byt and v[1] else {})}
+               for k, v in phases.items()}
+    solver.close()
+    del solver
+
+    # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hostA = [a.cpu().pin_memory() for a in P.A]
+        hostb = [b.cpu().pin_memory() for b in P.b]
+        del P
+        torch.cuda.empty_cache()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dA = [a.to("cuda", non_blocking=True) for a in hostA]
+        db = [b.to("cuda", non_blocking=True) for b in hostb]
+        b_all2 = [None] * N
+        blocks2 = []
+        for k in range(nl):
+            b_all2[rank * nl + k] = db[k]
+            blocks2.append((rank * nl + k, 0, dA[k]))
+        s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False)
+        for _ in range(args.steps):
+            s2.iterate(1)          # each step reads back its 6 residual scalars
+        z = s2.z                   # D2H of the result
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = sum(a.numel() * a.element_size() for a in hostA) + sum(b.numel() * b.element_size() for b in hostb)
+        e2e = {"value": N * sweeps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int((6 * 8 * args.steps + z.nbytes) / args.steps),
+               "ms_total": ems, "includes": "H2D of A,b + setup (Gram+factor) + steps + D2H of z"}
+        s2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        o = oracle_sample(args.cpu_m, args.cpu_n, args.inner, 2, 1, n, m)
+        cpu = {"value": o["value"] * N / nl if False else o["value"], "unit": UNIT, "cores": o["cores"],
+               "kind": "oracle", "sample": o["sample"]}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded, P:268 recipe; DESIGN.md 5)",
+            "config": {"workload": WORKLOAD if (args.n, args.m, args.nodes, args.loss) == (10_000, 25_000, 4, "logistic")
+                       else f"custom: {args.loss}, {nl} nodes/rank x m_i={m}, n={n}, kappa={args.kappa}",
+                       "nodes_total": N, "nodes_per_rank": nl, "m_i": m, "n": n, "kappa": args.kappa,
+                       "K_in": args.inner, "placement": "node-major" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (A = %.1f GB/rank)" % (A_bytes / 1e9),
+                       "sweeps_per_s": sweeps / (ms / 1e3), "setup_wall_s": setup_wall},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "residuals_last": sc,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    t0 = time.time()
+    o = oracle_sample(args.cpu_m, args.cpu_n, args.inner, args.steps, args.warmup, args.n, args.m)
+    value = o["value"]
+    ms_per_step = args.inner * 1e3 / value
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, P:268 recipe)",
+        "config": {"workload": WORKLOAD, "K_in": args.inner},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": o["cores"], "kind": "oracle", "sample": o["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

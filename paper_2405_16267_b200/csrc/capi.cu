@@ -1,0 +1,918 @@
+// capi.cu -- the C ABI of libbicadmm (include/bicadmm.h): handle, workspace
+// plan, one-time setup, the outer/inner iteration driver, finalize, NCCL comm.
+//
+// Iteration order (Eq. (7) order, DESIGN R2), per outer iteration k:
+//   Algorithm 2, K_in sweeps for every local node:
+//      a1+a2  gemv_t : r_ij = rho_l A_ij^T (p_ij + delta_i) + rho_c (z_j - u_ij)
+//      a3     gemv   : x_ij = H_ij r_ij
+//      a4     gemv   : p_ij = A_ij x_ij
+//      a5     block sum (+ NCCL AllReduce over the node group when blocks span GPUs)
+//      a6+a7  prox   : abar, omega_bar (22), nu (23), delta
+//   Algorithm 1, replicated on every rank:
+//      a9  Collect   : wsum = sum_i (x_i + u_i) (+ NCCL AllReduce over all ranks)
+//      a10 (7b)      : z, t
+//      a11 (13)      : s
+//      a12 (14)      : v;  (9) u_i += x_i - z;  (15) p_r, d_r, b_r -> host (one sync)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/bicadmm.h"
+#include "../../include/bicadmm_ops.h"
+#include "common.cuh"
+#include "kernels.h"
+
+#if __has_include(<nccl.h>)
+#include <nccl.h>
+#define BIC_HAVE_NCCL 1
+#else
+#define BIC_HAVE_NCCL 0
+#endif
+
+using namespace bic;
+
+// ======================================================================= NCCL (dlopen)
+namespace {
+#if BIC_HAVE_NCCL
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+        CommSplit = (decltype(CommSplit))dlsym(h, "ncclCommSplit");
+        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        CommCount = (decltype(CommCount))dlsym(h, "ncclCommCount");
+        return GetUniqueId && CommInitRank && CommSplit && AllReduce && CommDestroy && CommCount;
+    }
+};
+NcclApi g_nccl;
+#endif
+}  // namespace
+
+struct bicadmm_comm {
+    int world = 1, rank = 0, device = 0, color = 0, group_size = 1;
+#if BIC_HAVE_NCCL
+    ncclComm_t world_comm = nullptr, group_comm = nullptr;
+#endif
+};
+
+// ======================================================================= handle
+namespace {
+
+struct LBlock {      // a local block (i, j), sorted by (node, block)
+    int node, block, user_index, li, jl;
+    const void* A;
+    int64_t lda, m, c0, nj;
+    void* H;
+    int64_t ldh;
+    double *x, *u, *r, *p, *partial, *pobj;
+};
+struct LNode {
+    int node, li;
+    int64_t m;
+    const void* b;
+    double *nu, *delta, *S, *p_base, *pobj_base, *sq_partial, *obj_partial;
+    int np;
+    int64_t nprox_ctas;
+};
+
+struct Bump {  // 256-byte aligned bump allocator over the workspace (base may be null to size)
+    char* base;
+    size_t off = 0;
+    explicit Bump(void* b) : base((char*)b) {}
+    void* take(size_t bytes) {
+        off = (off + 255) / 256 * 256;
+        void* p = base ? base + off : nullptr;
+        off += bytes;
+        return p;
+    }
+    template <typename T> T* arr(int64_t n) { return (T*)take(sizeof(T) * (size_t)(n > 0 ? n : 1)); }
+};
+
+int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+struct bicadmm_handle {
+    // problem
+    int N = 0, M = 0, C = 1, loss = 0, dtype = 0;
+    int64_t n = 0, len = 0, lenp = 0;   // lenp: 64-byte aligned per-node stride of x_all / u_all
+    std::vector<int64_t> m, col_start;
+    bicadmm_params prm{};
+    bicadmm_comm* comm = nullptr;
+    bool split_blocks = false;  // some node's blocks live on other ranks
+    cudaStream_t st = nullptr;
+    int sm_count = 148, gemv_cap = 148;
+    size_t ws_bytes = 0;
+    // layout
+    std::vector<LBlock> blk;
+    std::vector<LNode> nod;
+    double *x_all = nullptr, *u_all = nullptr, *z = nullptr, *z_prev = nullptr, *s = nullptr, *wbar = nullptr,
+           *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
+           *fws = nullptr, *node_obj = nullptr;
+    OuterScalars* sc = nullptr;
+    int64_t* support = nullptr;
+    int64_t* support_count = nullptr;
+    // launch descriptors
+    std::vector<GemvTDesc> gt;
+    std::vector<BlockVec> bv;
+    // host state
+    OuterScalars* host_sc = nullptr;  // pinned
+    int64_t* host_i64 = nullptr;      // pinned
+    int outer_done = 0;
+    int64_t inner_total = 0;
+    std::vector<std::array<double, 6>> trace;
+    std::vector<int32_t> inner_counts;
+    std::vector<int32_t> schedule;
+    int sched_start = 0, sched_rows = 0;
+    bool dead = false, finalized = false, converged = false;
+    int64_t support_len = 0;
+    double objective = 0.0, ms_setup = 0.0, ms_solve = 0.0;
+    int64_t launches0 = 0;
+    std::string err;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // per-phase profiling (bicadmm_set_profiling)
+    bool prof = false;
+    std::vector<cudaEvent_t> evpool;
+    size_t evused = 0;
+    struct Pending { int phase; cudaEvent_t a, b; int64_t launches; };
+    std::vector<Pending> pending;
+    double phase_ms[BICADMM_NPHASE] = {};
+    int64_t phase_cnt[BICADMM_NPHASE] = {};
+};
+
+static cudaEvent_t next_event(bicadmm_handle* h) {
+    if (h->evused == h->evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->evpool.push_back(e);
+    }
+    return h->evpool[h->evused++];
+}
+
+// Resolve recorded phase events (call only after the stream has been synchronised).
+static void resolve_phases(bicadmm_handle* h) {
+    for (auto& p : h->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) h->phase_ms[p.phase] += ms;
+        h->phase_cnt[p.phase] += p.launches;
+    }
+    h->pending.clear();
+    h->evused = 0;
+}
+
+static int fail(bicadmm_handle* h, int rc, const std::string& msg) {
+    if (h) {
+        h->err = msg;
+        if (rc == BICADMM_ERR_CUDA || rc == BICADMM_ERR_NCCL) h->dead = true;
+    }
+    return rc;
+}
+
+#define H_CUDA(h, expr)                                                                                \
+    do {                                                                                               \
+        cudaError_t _e = (expr);                                                                       \
+        if (_e != cudaSuccess) return fail(h, BICADMM_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+    } while (0)
+#define H_RC(h, expr)                                                                                  \
+    do {                                                                                               \
+        int _r = (expr);                                                                               \
+        if (_r != BICADMM_OK) {                                                                        \
+            if (_r == BICADMM_ERR_CUDA) return fail(h, _r, std::string(#expr ": ") + cudaGetErrorString(cudaGetLastError())); \
+            return fail(h, _r, #expr);                                                                 \
+        }                                                                                              \
+    } while (0)
+
+// ----------------------------------------------------------------------- validation
+static int validate(const bicadmm_problem* P, const bicadmm_params* R, std::string* why) {
+    if (!P || !R || !P->m || !P->col_start || (P->n_blocks > 0 && !P->blocks) || !P->b) { *why = "null pointer"; return BICADMM_ERR_INVALID; }
+    if (P->N < 1 || P->M < 1 || P->n < 1 || P->C < 1) { *why = "N, M, n, C must be >= 1"; return BICADMM_ERR_DIM; }
+    if (P->loss < 0 || P->loss > 3) { *why = "unknown loss"; return BICADMM_ERR_INVALID; }
+    if (P->dtype != BICADMM_F64 && P->dtype != BICADMM_F32) { *why = "unknown dtype"; return BICADMM_ERR_INVALID; }
+    if ((P->loss == BICADMM_SOFTMAX) != (P->C > 1)) { *why = "C > 1 iff softmax"; return BICADMM_ERR_DIM; }
+    if (P->C > 1) { *why = "softmax (C > 1) is not supported by this build's GPU path yet"; return BICADMM_ERR_INVALID; }
+    if (P->col_start[0] != 0 || P->col_start[P->M] != P->n) { *why = "col_start must span [0, n]"; return BICADMM_ERR_DIM; }
+    for (int j = 0; j < P->M; ++j) {
+        if (P->col_start[j + 1] <= P->col_start[j]) { *why = "col_start not increasing"; return BICADMM_ERR_DIM; }
+        if (P->col_start[j] % 4) { *why = "col_start[j] must be a multiple of 4"; return BICADMM_ERR_INVALID; }
+    }
+    for (int i = 0; i < P->N; ++i) if (P->m[i] < 1) { *why = "m_i must be >= 1"; return BICADMM_ERR_DIM; }
+    if (P->n_blocks < 1) { *why = "no local blocks"; return BICADMM_ERR_PLACEMENT; }
+    std::vector<char> seen((size_t)P->N * P->M, 0);
+    for (int k = 0; k < P->n_blocks; ++k) {
+        const bicadmm_block& b = P->blocks[k];
+        if (b.node < 0 || b.node >= P->N || b.block < 0 || b.block >= P->M) { *why = "block id out of range"; return BICADMM_ERR_PLACEMENT; }
+        if (seen[(size_t)b.node * P->M + b.block]++) { *why = "duplicate block"; return BICADMM_ERR_PLACEMENT; }
+        const int64_t nj = P->col_start[b.block + 1] - P->col_start[b.block];
+        if (!b.A) { *why = "null block pointer"; return BICADMM_ERR_INVALID; }
+        if (b.lda < nj || b.lda % 4 || ((uintptr_t)b.A) % 16) { *why = "A must be 16-byte aligned with lda >= n_j, lda % 4 == 0"; return BICADMM_ERR_INVALID; }
+        if (!P->b[b.node]) { *why = "missing labels for a node with a local block"; return BICADMM_ERR_PLACEMENT; }
+    }
+    if (R->kappa < 0 || R->kappa > P->n * P->C) { *why = "kappa outside [0, n*C]"; return BICADMM_ERR_INVALID; }
+    if (!(R->rho_c > 0) || !(R->rho_l > 0) || !(R->lambda > 0)) { *why = "penalties must be > 0"; return BICADMM_ERR_INVALID; }
+    if (!(R->alpha > 0 && R->alpha <= 1)) { *why = "alpha must be in (0, 1]"; return BICADMM_ERR_INVALID; }
+    if (R->eps_p < 0 || R->eps_d < 0 || R->eps_b < 0 || R->eps_inner < 0) { *why = "tolerances must be >= 0"; return BICADMM_ERR_INVALID; }
+    if (R->inner_fixed < 0 || (R->inner_fixed == 0 && R->max_inner < 1)) { *why = "inner schedule"; return BICADMM_ERR_INVALID; }
+    return BICADMM_OK;
+}
+
+// Layout of the workspace (also used to size it).  Returns bytes.
+static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
+    Bump b(base);
+    const int C = P->C;
+    const int64_t len = P->n * C;
+    const int64_t lenp = rup(len, 8);
+    h->lenp = lenp;
+    h->blk.clear();
+    h->nod.clear();
+    for (int k = 0; k < P->n_blocks; ++k) {
+        LBlock L{};
+        L.node = P->blocks[k].node;
+        L.block = P->blocks[k].block;
+        L.user_index = k;
+        L.A = P->blocks[k].A;
+        L.lda = P->blocks[k].lda;
+        L.m = P->m[L.node];
+        L.c0 = P->col_start[L.block];
+        L.nj = P->col_start[L.block + 1] - L.c0;
+        h->blk.push_back(L);
+    }
+    std::sort(h->blk.begin(), h->blk.end(), [](const LBlock& a, const LBlock& c) {
+        return a.node != c.node ? a.node < c.node : a.block < c.block;
+    });
+    for (auto& L : h->blk) {
+        if (h->nod.empty() || h->nod.back().node != L.node) {
+            LNode nd{};
+            nd.node = L.node;
+            nd.li = (int)h->nod.size();
+            nd.m = L.m;
+            nd.b = P->b[L.node];
+            h->nod.push_back(nd);
+        }
+        L.li = h->nod.back().li;
+        L.jl = h->nod.back().np++;
+    }
+    const int nl = (int)h->nod.size();
+    int64_t njmax = 0;
+    for (auto& L : h->blk) njmax = std::max(njmax, L.nj);
+    // matrices
+    const size_t es = P->dtype == BICADMM_F64 ? 8 : 4;
+    for (auto& L : h->blk) {
+        L.ldh = rup(L.nj, 4);
+        L.H = b.take(es * (size_t)(L.ldh * L.nj));
+    }
+    // global vectors
+    h->x_all = b.arr<double>(lenp * nl);
+    h->u_all = b.arr<double>(lenp * nl);
+    h->z = b.arr<double>(len);
+    h->z_prev = b.arr<double>(len);
+    h->s = b.arr<double>(len);
+    h->wbar = b.arr<double>(len);
+    h->wsum = b.arr<double>(len);
+    h->x_final = b.arr<double>(len);
+    h->node_sq = b.arr<double>(P->N);
+    h->node_obj = b.arr<double>(P->N);
+    h->sc = b.arr<OuterScalars>(1);
+    h->support = b.arr<int64_t>(P->n * C);
+    h->support_count = b.arr<int64_t>(1);
+    int64_t uparts = 0;
+    for (auto& L : h->blk) uparts += (L.nj * C + kUThreads * 4 - 1) / (kUThreads * 4);
+    h->upart = b.arr<double>(uparts);
+    // per node
+    for (auto& nd : h->nod) {
+        nd.nu = b.arr<double>(nd.m * C);
+        nd.delta = b.arr<double>(nd.m * C);
+        nd.S = b.arr<double>(nd.m * C);
+        nd.p_base = b.arr<double>(nd.m * C * nd.np);
+        nd.pobj_base = b.arr<double>(nd.m * C * nd.np);
+        nd.nprox_ctas = (nd.m + kProxThreads - 1) / kProxThreads;
+        nd.sq_partial = b.arr<double>(nd.nprox_ctas);
+        nd.obj_partial = b.arr<double>(nd.nprox_ctas);
+    }
+    // per block vectors + gemv_t scratch
+    h->gt.assign(h->blk.size(), GemvTDesc{});
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        h->gt[k].rows = h->blk[k].m;
+        h->gt[k].cols = h->blk[k].nj;
+    }
+    std::vector<int64_t> need(h->blk.size());
+    plan_gemv_t(P->dtype, h->gt.data(), (int)h->gt.size(), h->sm_count, need.data());
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        LBlock& L = h->blk[k];
+        LNode& nd = h->nod[L.li];
+        L.x = h->x_all + (base ? (int64_t)L.li * lenp + L.c0 * C : 0);
+        L.u = h->u_all + (base ? (int64_t)L.li * lenp + L.c0 * C : 0);
+        L.p = nd.p_base + (base ? (int64_t)L.jl * nd.m * C : 0);
+        L.r = b.arr<double>(L.nj * C);
+        L.pobj = nd.pobj_base + (base ? (int64_t)L.jl * nd.m * C : 0);
+        L.partial = b.arr<double>(need[k]);
+    }
+    // setup scratch: FP64 Gram / factor workspace
+    const int64_t ldg = rup(njmax, 8);
+    h->gram = b.arr<double>(ldg * njmax);
+    h->fws = b.arr<double>((int64_t)factor_ws_doubles(njmax));
+    return b.off + 256;
+}
+
+static void build_descs(bicadmm_handle* h) {
+    const int C = h->C;
+    (void)C;
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        LBlock& L = h->blk[k];
+        GemvTDesc& g = h->gt[k];
+        g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
+        g.p = L.p; g.delta = h->nod[L.li].delta;
+        g.z = h->z + L.c0; g.u = L.u; g.r = L.r; g.partial = L.partial;
+    }
+    h->bv.clear();
+    for (auto& L : h->blk) {
+        BlockVec v{};
+        v.x = L.x; v.u = L.u; v.c0 = L.c0 * h->C; v.len = L.nj * h->C; v.node = L.node;
+        h->bv.push_back(v);
+    }
+}
+
+// ======================================================================= ABI: misc
+extern "C" {
+
+int bicadmm_version(void) { return BICADMM_ABI_VERSION; }
+
+const char* bicadmm_rc_string(int rc) {
+    switch (rc) {
+    case BICADMM_OK: return "ok";
+    case BICADMM_ERR_INVALID: return "invalid argument";
+    case BICADMM_ERR_DIM: return "dimension mismatch";
+    case BICADMM_ERR_DOMAIN: return "label outside the loss domain";
+    case BICADMM_ERR_PLACEMENT: return "invalid block placement";
+    case BICADMM_ERR_OOM: return "workspace too small";
+    case BICADMM_ERR_CUDA: return "CUDA error";
+    case BICADMM_ERR_NCCL: return "NCCL error";
+    case BICADMM_ERR_STATE: return "invalid handle state";
+    }
+    return "unknown";
+}
+
+int64_t bicadmm_launch_count(void) { return g_launches.load(); }
+
+int bicadmm_uid_size(void) {
+#if BIC_HAVE_NCCL
+    return (int)sizeof(ncclUniqueId);
+#else
+    return 128;
+#endif
+}
+
+int bicadmm_get_unique_id(void* uid_out) {
+#if BIC_HAVE_NCCL
+    if (!uid_out) return BICADMM_ERR_INVALID;
+    if (!g_nccl.load()) return BICADMM_ERR_NCCL;
+    ncclUniqueId id;
+    if (g_nccl.GetUniqueId(&id) != ncclSuccess) return BICADMM_ERR_NCCL;
+    memcpy(uid_out, &id, sizeof(id));
+    return BICADMM_OK;
+#else
+    (void)uid_out;
+    return BICADMM_ERR_NCCL;
+#endif
+}
+
+int bicadmm_comm_init(int world, int rank, int device, const void* uid, int group_color, bicadmm_comm** out) {
+    if (!out || world < 1 || rank < 0 || rank >= world || group_color < 0) return BICADMM_ERR_INVALID;
+    bicadmm_comm* c = new bicadmm_comm();
+    c->world = world; c->rank = rank; c->device = device; c->color = group_color;
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; return BICADMM_ERR_CUDA; }
+    if (world > 1) {
+#if BIC_HAVE_NCCL
+        if (!uid || !g_nccl.load()) { delete c; return BICADMM_ERR_NCCL; }
+        ncclUniqueId id;
+        memcpy(&id, uid, sizeof(id));
+        if (g_nccl.CommInitRank(&c->world_comm, world, id, rank) != ncclSuccess) { delete c; return BICADMM_ERR_NCCL; }
+        if (g_nccl.CommSplit(c->world_comm, group_color, rank, &c->group_comm, nullptr) != ncclSuccess) {
+            g_nccl.CommDestroy(c->world_comm);
+            delete c;
+            return BICADMM_ERR_NCCL;
+        }
+        g_nccl.CommCount(c->group_comm, &c->group_size);
+#else
+        delete c;
+        return BICADMM_ERR_NCCL;
+#endif
+    }
+    *out = c;
+    return BICADMM_OK;
+}
+
+int bicadmm_comm_destroy(bicadmm_comm* c) {
+    if (!c) return BICADMM_OK;
+#if BIC_HAVE_NCCL
+    if (c->group_comm) g_nccl.CommDestroy(c->group_comm);
+    if (c->world_comm) g_nccl.CommDestroy(c->world_comm);
+#endif
+    delete c;
+    return BICADMM_OK;
+}
+
+int bicadmm_workspace_size(const bicadmm_problem* P, const bicadmm_params* R, size_t* bytes) {
+    std::string why;
+    if (!bytes) return BICADMM_ERR_INVALID;
+    int rc = validate(P, R, &why);
+    if (rc) return rc;
+    bicadmm_handle tmp;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&tmp.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) tmp.sm_count = 148;
+    tmp.C = P->C;
+    *bytes = plan(&tmp, P, nullptr);
+    return BICADMM_OK;
+}
+
+}  // extern "C"
+
+// ======================================================================= collectives
+static int allreduce(bicadmm_handle* h, double* buf, int64_t count, bool group) {
+#if BIC_HAVE_NCCL
+    if (!h->comm || h->comm->world == 1 || count <= 0) return BICADMM_OK;
+    ncclComm_t c = group ? h->comm->group_comm : h->comm->world_comm;
+    if (group && h->comm->group_size == 1) return BICADMM_OK;
+    if (g_nccl.AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, c, h->st) != ncclSuccess)
+        return fail(h, BICADMM_ERR_NCCL, "ncclAllReduce");
+    return BICADMM_OK;
+#else
+    (void)buf; (void)count; (void)group;
+    return h->comm && h->comm->world > 1 ? fail(h, BICADMM_ERR_NCCL, "built without NCCL") : BICADMM_OK;
+#endif
+}
+
+// ======================================================================= setup
+extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, bicadmm_comm* comm, void* ws,
+                             size_t ws_bytes, void* stream, bicadmm_handle** out) {
+    if (!out) return BICADMM_ERR_INVALID;
+    *out = nullptr;
+    std::string why;
+    int rc = validate(P, R, &why);
+    if (rc) return rc;
+    bicadmm_handle* h = new bicadmm_handle();
+    h->N = P->N; h->M = P->M; h->C = P->C; h->loss = P->loss; h->dtype = P->dtype;
+    h->n = P->n; h->len = P->n * P->C;
+    h->m.assign(P->m, P->m + P->N);
+    h->col_start.assign(P->col_start, P->col_start + P->M + 1);
+    h->prm = *R;
+    h->comm = comm;
+    h->st = (cudaStream_t)stream;
+    h->launches0 = g_launches.load();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    h->gemv_cap = gemv_grid_cap(P->dtype, h->sm_count);
+    const size_t need = plan(h, P, nullptr);
+    if (!ws || ws_bytes < need) { delete h; return BICADMM_ERR_OOM; }
+    if (((uintptr_t)ws) % 256) { delete h; return BICADMM_ERR_INVALID; }
+    plan(h, P, ws);
+    h->ws_bytes = ws_bytes;
+    if (comm && comm->world > 1) {
+        // a node whose M blocks are not all local has its block sum all-reduced per sweep
+        for (auto& nd : h->nod) if (nd.np != P->M) h->split_blocks = true;
+        if (h->split_blocks && comm->group_size * 1 < 2) { delete h; return BICADMM_ERR_PLACEMENT; }
+    } else {
+        for (auto& nd : h->nod) if (nd.np != P->M) { delete h; return BICADMM_ERR_PLACEMENT; }
+        if ((int)h->nod.size() != P->N) { delete h; return BICADMM_ERR_PLACEMENT; }
+    }
+    build_descs(h);
+    // validate labels on the host side?  Labels are device memory: check them on device
+    // with the loss kernel path is costly; the domain check is done in the Python binding.
+    if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
+        cudaMallocHost(&h->host_i64, sizeof(int64_t) * 4) != cudaSuccess) {
+        bicadmm_destroy(h);
+        return BICADMM_ERR_CUDA;
+    }
+    cudaEventCreate(&h->e0);
+    cudaEventCreate(&h->e1);
+    // zero all state (DESIGN R10)
+    const int C = h->C;
+    const int64_t len = h->len;
+    const int nl = (int)h->nod.size();
+    auto zero = [&](void* p, size_t bytes) { return cudaMemsetAsync(p, 0, bytes, h->st); };
+    if (zero(h->x_all, sizeof(double) * h->lenp * nl) || zero(h->u_all, sizeof(double) * h->lenp * nl) ||
+        zero(h->z, sizeof(double) * len) || zero(h->z_prev, sizeof(double) * len) ||
+        zero(h->s, sizeof(double) * len) || zero(h->wbar, sizeof(double) * len) ||
+        zero(h->x_final, sizeof(double) * len) || zero(h->sc, sizeof(OuterScalars))) {
+        int r2 = fail(h, BICADMM_ERR_CUDA, "memset");
+        bicadmm_destroy(h);
+        return r2;
+    }
+    for (auto& nd : h->nod) {
+        if (zero(nd.nu, sizeof(double) * nd.m * C) || zero(nd.delta, sizeof(double) * nd.m * C) ||
+            zero(nd.p_base, sizeof(double) * nd.m * C * nd.np) || zero(nd.S, sizeof(double) * nd.m * C)) {
+            bicadmm_destroy(h);
+            return BICADMM_ERR_CUDA;
+        }
+    }
+    // one-time block factors (a0)
+    cudaEventRecord(h->e0, h->st);
+    const double c = R->lambda / (double)P->N + R->rho_c;   // 1/(N gamma) + rho_c
+    for (auto& L : h->blk) {
+        const int64_t ldg = rup(L.nj, 8);
+        rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, h->gram, ldg, false, h->st);
+        if (!rc) rc = factor_inverse(L.nj, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
+        if (rc) {
+            std::string msg = rc == BICADMM_ERR_CUDA ? std::string("factor: ") + cudaGetErrorString(cudaGetLastError())
+                                                     : std::string("factor: matrix not positive definite");
+            fail(h, rc, msg);
+            fprintf(stderr, "bicadmm_setup: %s\n", msg.c_str());
+            bicadmm_destroy(h);
+            return rc;
+        }
+    }
+    cudaEventRecord(h->e1, h->st);
+    if (cudaEventSynchronize(h->e1) != cudaSuccess) { bicadmm_destroy(h); return BICADMM_ERR_CUDA; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->e0, h->e1);
+    h->ms_setup = ms;
+    *out = h;
+    return BICADMM_OK;
+}
+
+// ======================================================================= iterate
+static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes) {
+    // descriptors for the active nodes' blocks
+    std::vector<GemvTDesc> gt;
+    std::vector<GemvDesc> hx, ax;
+    std::vector<ProxNode> px;
+    std::vector<char> act(h->nod.size(), 0);
+    for (int li : active_nodes) act[li] = 1;
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        const LBlock& L = h->blk[k];
+        if (!act[L.li]) continue;
+        gt.push_back(h->gt[k]);
+        GemvDesc d1{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0};
+        hx.push_back(d1);
+        GemvDesc d2{L.A, L.lda, L.m, L.nj, L.x, L.p, 0};
+        ax.push_back(d2);
+    }
+    for (int li : active_nodes) {
+        const LNode& nd = h->nod[li];
+        ProxNode p{};
+        p.b = nd.b; p.p = nd.p_base; p.S = h->split_blocks ? nd.S : nullptr; p.nu = nd.nu; p.delta = nd.delta;
+        p.omega = nullptr; p.sq_partial = nullptr; p.m = nd.m; p.pstride = nd.m * h->C; p.np = nd.np;
+        px.push_back(p);
+    }
+    cudaEvent_t ev[7] = {};
+    int64_t l0 = g_launches.load(), lc[7] = {};
+    auto mark = [&](int k) {
+        if (!h->prof) return;
+        ev[k] = next_event(h);
+        cudaEventRecord(ev[k], h->st);
+        lc[k] = g_launches.load();
+    };
+    mark(0);
+    cudaEvent_t mid = h->prof ? next_event(h) : nullptr;
+    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid));
+    const int64_t l_partial = (int64_t)(gt.size() + kMaxDesc - 1) / kMaxDesc;
+    mark(2);
+    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st));
+    mark(3);
+    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st));
+    mark(4);
+    if (h->split_blocks) {
+        H_RC(h, launch_psum(h->C, px.data(), (int)px.size(), nullptr, h->st));
+        // all local nodes' S are contiguous only per node: one AllReduce per node (batched by NCCL group)
+        for (int li : active_nodes) H_RC(h, allreduce(h, h->nod[li].S, h->nod[li].m * h->C, true));
+    }
+    mark(5);
+    H_RC(h, launch_prox(h->loss, h->dtype, h->C, h->M, h->prm.rho_l, px.data(), (int)px.size(), h->st));
+    mark(6);
+    if (h->prof) {
+        h->pending.push_back({0, ev[0], mid, l_partial});
+        h->pending.push_back({1, mid, ev[2], lc[2] - l0 - l_partial});
+        h->pending.push_back({2, ev[2], ev[3], lc[3] - lc[2]});
+        h->pending.push_back({3, ev[3], ev[4], lc[4] - lc[3]});
+        h->pending.push_back({4, ev[4], ev[5], lc[5] - lc[4]});
+        h->pending.push_back({5, ev[5], ev[6], lc[6] - lc[5]});
+    }
+    return BICADMM_OK;
+}
+
+static int outer_step(bicadmm_handle* h) {
+    const double rho_b = h->prm.alpha * h->prm.rho_c;
+    cudaEvent_t oa = nullptr, ob = nullptr;
+    const int64_t lo0 = g_launches.load();
+    if (h->prof) { oa = next_event(h); cudaEventRecord(oa, h->st); }
+    H_RC(h, launch_wsum(h->len, h->lenp, h->x_all, h->u_all, (int)h->nod.size(), h->wsum, h->st));
+    H_RC(h, allreduce(h, h->wsum, h->len, false));
+    H_RC(h, launch_zt(h->len, h->N, h->prm.rho_c, rho_b, h->wsum, h->s, h->wbar, h->z, h->z_prev, h->sc, h->st));
+    H_RC(h, launch_s_update(h->len, h->prm.kappa, h->z, h->s, h->sc, h->st));
+    H_RC(h, launch_u_update(h->bv.data(), (int)h->bv.size(), h->z, h->upart, h->st));
+    H_RC(h, launch_node_sq(h->bv.data(), (int)h->bv.size(), h->upart, h->N, h->node_sq, h->st));
+    if (h->comm && h->comm->world > 1) {
+        // every (i, j) contributes exactly once: node_sq partials are per local block
+        H_RC(h, allreduce(h, h->node_sq, h->N, false));
+    }
+    H_RC(h, launch_residuals(h->N, std::sqrt((double)h->N) * h->prm.rho_c, h->node_sq, h->sc, h->st));
+    if (h->prof) {
+        ob = next_event(h);
+        cudaEventRecord(ob, h->st);
+        h->pending.push_back({6, oa, ob, g_launches.load() - lo0});
+    }
+    H_CUDA(h, cudaMemcpyAsync(h->host_sc, h->sc, sizeof(OuterScalars), cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    if (h->prof) resolve_phases(h);
+    return BICADMM_OK;
+}
+
+static int sweeps_for(bicadmm_handle* h, int k, int li) {
+    if (!h->schedule.empty()) {
+        const int row = k - h->sched_start;
+        if (row >= 0 && row < h->sched_rows) return h->schedule[(size_t)row * h->N + h->nod[li].node];
+    }
+    return h->prm.inner_fixed > 0 ? h->prm.inner_fixed : h->prm.max_inner;
+}
+
+extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info* info) {
+    if (!h) return BICADMM_ERR_INVALID;
+    if (h->dead) return BICADMM_ERR_STATE;
+    if (n_outer < 0) return fail(h, BICADMM_ERR_INVALID, "n_outer < 0");
+    if (h->prm.inner_fixed == 0 && h->schedule.empty())
+        return fail(h, BICADMM_ERR_INVALID, "tolerance-mode inner loop is not implemented in this build; use inner_fixed > 0 or a schedule");
+    int sweeps_call = 0;
+    for (int it = 0; it < n_outer; ++it) {
+        const int k = h->outer_done;
+        std::vector<int> want(h->nod.size());
+        int maxs = 0;
+        for (size_t li = 0; li < h->nod.size(); ++li) {
+            want[li] = sweeps_for(h, k, (int)li);
+            maxs = std::max(maxs, want[li]);
+        }
+        for (int sw = 0; sw < maxs; ++sw) {
+            std::vector<int> active;
+            for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);
+            int rc = inner_sweep(h, active);
+            if (rc) return rc;
+        }
+        int rc = outer_step(h);
+        if (rc) return rc;
+        const OuterScalars& s = *h->host_sc;
+        h->trace.push_back({s.p_r, s.d_r, s.b_r, s.t, s.v, s.tau});
+        std::vector<int32_t> row(h->N, 0);
+        for (size_t li = 0; li < h->nod.size(); ++li) row[h->nod[li].node] = want[li];
+        h->inner_counts.insert(h->inner_counts.end(), row.begin(), row.end());
+        h->outer_done++;
+        h->inner_total += maxs;
+        sweeps_call += maxs;
+        h->converged = s.p_r <= h->prm.eps_p && s.d_r <= h->prm.eps_d && s.b_r <= h->prm.eps_b;
+        h->finalized = false;
+    }
+    if (info) {
+        info->outer_iters = h->outer_done;
+        info->inner_sweeps = sweeps_call;
+        const OuterScalars& s = *h->host_sc;
+        info->p_r = s.p_r; info->d_r = s.d_r; info->b_r = s.b_r;
+        info->t = s.t; info->v = s.v; info->tau = s.tau;
+        info->converged = h->converged ? 1 : 0;
+    }
+    return BICADMM_OK;
+}
+
+// ======================================================================= finalize
+__global__ void k_scatter_support(const double* __restrict__ z, const int64_t* __restrict__ sup,
+                                  const int64_t* __restrict__ cnt, double* __restrict__ xf) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < *cnt) xf[sup[k]] = z[sup[k]];
+}
+__global__ void k_sum_partials(const double* __restrict__ parts, int64_t n, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int64_t k = 0; k < n; ++k) s += parts[k];
+        *out = s;
+    }
+}
+__global__ void k_sqnorm(int64_t len, const double* __restrict__ x, double* out) {
+    __shared__ double scratch[32];
+    double a = 0.0;
+    for (int64_t l = threadIdx.x; l < len; l += blockDim.x) a += x[l] * x[l];
+    a = block_sum(a, scratch);
+    if (threadIdx.x == 0) *out = a;
+}
+
+// Support = top-kappa of |z| with z != 0 (ties to the lower index), x_final = z on
+// the support (DESIGN R19), objective (1) at x_final (DESIGN R20).
+static int do_finalize(bicadmm_handle* h) {
+    const int64_t len = h->len;
+    if (h->prm.refit && h->loss == BICADMM_LS)
+        return fail(h, BICADMM_ERR_INVALID, "LS refit on the support is not implemented in this build's GPU path; pass refit = 0");
+    H_RC(h, launch_support(len, h->prm.kappa, h->z, h->support, h->support_count, h->st));
+    H_CUDA(h, cudaMemsetAsync(h->x_final, 0, sizeof(double) * len, h->st));
+    const int64_t kk = std::max<int64_t>(1, std::min<int64_t>(h->prm.kappa, len));
+    k_scatter_support<<<(unsigned)((kk + 255) / 256), 256, 0, h->st>>>(h->z, h->support, h->support_count, h->x_final);
+    BIC_LAUNCHED();
+    // data term per node from p = sum_j A_ij x_final_j
+    std::vector<GemvDesc> ax;
+    for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0});
+    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st));
+    std::vector<ProxNode> px;
+    for (auto& nd : h->nod) {
+        ProxNode p{};
+        p.b = nd.b; p.m = nd.m; p.p = nd.pobj_base; p.pstride = nd.m * h->C; p.np = nd.np;
+        p.sq_partial = nd.obj_partial;
+        if (h->split_blocks) {
+            p.S = nd.S;
+            H_RC(h, launch_psum(h->C, &p, 1, nullptr, h->st));
+            H_RC(h, allreduce(h, nd.S, nd.m * h->C, true));
+        }
+        px.push_back(p);
+    }
+    H_RC(h, launch_loss(h->loss, h->dtype, h->C, px.data(), (int)px.size(), h->st));
+    H_CUDA(h, cudaMemsetAsync(h->node_obj, 0, sizeof(double) * h->N, h->st));
+    for (auto& nd : h->nod) {
+        k_sum_partials<<<1, 32, 0, h->st>>>(nd.obj_partial, nd.nprox_ctas, h->node_obj + nd.node);
+        BIC_LAUNCHED();
+    }
+    // a node's loss is replicated on every rank of its group; the world sum divided by the
+    // group size restores it (group sizes are powers of two in every placement we build)
+    H_RC(h, allreduce(h, h->node_obj, h->N, false));
+    k_sqnorm<<<1, 1024, 0, h->st>>>(len, h->x_final, h->wsum);
+    BIC_LAUNCHED();
+    H_CUDA(h, cudaMemcpyAsync(h->host_i64, h->support_count, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+    std::vector<double> nobj(h->N + 1);
+    H_CUDA(h, cudaMemcpyAsync(nobj.data(), h->node_obj, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaMemcpyAsync(nobj.data() + h->N, h->wsum, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    double obj = 0.0;
+    const double gs = (h->comm && h->comm->world > 1 && h->split_blocks) ? (double)h->comm->group_size : 1.0;
+    for (int i = 0; i < h->N; ++i) obj += nobj[i] / gs;
+    obj += 0.5 * h->prm.lambda * nobj[h->N];
+    h->objective = obj;
+    h->support_len = h->host_i64[0];
+    h->finalized = true;
+    return BICADMM_OK;
+}
+
+static void fill_report(bicadmm_handle* h, bicadmm_report* rep) {
+    if (!rep) return;
+    rep->converged = h->converged;
+    rep->outer_iters = h->outer_done;
+    rep->inner_sweeps = h->inner_total;
+    rep->support_len = h->support_len;
+    rep->objective = h->objective;
+    const OuterScalars& s = *h->host_sc;
+    rep->p_r = s.p_r; rep->d_r = s.d_r; rep->b_r = s.b_r;
+    rep->ms_setup = h->ms_setup;
+    rep->ms_solve = h->ms_solve;
+}
+
+extern "C" int bicadmm_finalize(bicadmm_handle* h, bicadmm_report* rep) {
+    if (!h) return BICADMM_ERR_INVALID;
+    if (h->dead) return BICADMM_ERR_STATE;
+    int rc = do_finalize(h);
+    if (rc) return rc;
+    fill_report(h, rep);
+    return BICADMM_OK;
+}
+
+extern "C" int bicadmm_solve(bicadmm_handle* h, bicadmm_report* rep) {
+    if (!h) return BICADMM_ERR_INVALID;
+    if (h->dead) return BICADMM_ERR_STATE;
+    H_CUDA(h, cudaEventRecord(h->e0, h->st));
+    while (!h->converged && h->outer_done < h->prm.max_outer) {
+        int rc = bicadmm_iterate(h, 1, nullptr);
+        if (rc) return rc;
+    }
+    int rc = do_finalize(h);
+    if (rc) return rc;
+    H_CUDA(h, cudaEventRecord(h->e1, h->st));
+    H_CUDA(h, cudaEventSynchronize(h->e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->e0, h->e1);
+    h->ms_solve = ms;
+    fill_report(h, rep);
+    return BICADMM_OK;
+}
+
+extern "C" int bicadmm_set_schedule(bicadmm_handle* h, const int32_t* counts, int n_rows) {
+    if (!h || (n_rows > 0 && !counts) || n_rows < 0) return BICADMM_ERR_INVALID;
+    for (int64_t k = 0; k < (int64_t)n_rows * h->N; ++k)
+        if (counts[k] < 0) return fail(h, BICADMM_ERR_INVALID, "negative sweep count");
+    h->schedule.assign(counts, counts + (size_t)n_rows * h->N);
+    h->sched_start = h->outer_done;
+    h->sched_rows = n_rows;
+    return BICADMM_OK;
+}
+
+// ======================================================================= get / destroy
+extern "C" int bicadmm_get(bicadmm_handle* h, int field, void* dst, size_t bytes, int on_device, size_t* bytes_out) {
+    if (!h) return BICADMM_ERR_INVALID;
+    const int64_t len = h->len;
+    size_t sz = 0;
+    const void* src = nullptr;
+    bool host_src = false;
+    std::vector<double> tmp;
+    std::vector<const void*> pieces;
+    std::vector<size_t> piece_sz;
+    switch (field) {
+    case BICADMM_FIELD_Z: sz = sizeof(double) * len; src = h->z; break;
+    case BICADMM_FIELD_S: sz = sizeof(double) * len; src = h->s; break;
+    case BICADMM_FIELD_WBAR: sz = sizeof(double) * len; src = h->wbar; break;
+    case BICADMM_FIELD_X_FINAL: sz = sizeof(double) * len; src = h->x_final; break;
+    case BICADMM_FIELD_SCALARS: {
+        const OuterScalars& s = *h->host_sc;
+        tmp = {s.t, s.v, s.tau, s.p_r, s.d_r, s.b_r};
+        sz = sizeof(double) * 6; src = tmp.data(); host_src = true;
+        break;
+    }
+    case BICADMM_FIELD_X_LOCAL:
+    case BICADMM_FIELD_U_LOCAL: {
+        std::vector<const LBlock*> order(h->blk.size());
+        for (auto& L : h->blk) order[L.user_index] = &L;
+        for (auto* L : order) {
+            pieces.push_back(field == BICADMM_FIELD_X_LOCAL ? L->x : L->u);
+            piece_sz.push_back(sizeof(double) * L->nj * h->C);
+            sz += piece_sz.back();
+        }
+        break;
+    }
+    case BICADMM_FIELD_NU:
+        for (auto& nd : h->nod) { pieces.push_back(nd.nu); piece_sz.push_back(sizeof(double) * nd.m * h->C); sz += piece_sz.back(); }
+        break;
+    case BICADMM_FIELD_SUPPORT: sz = sizeof(int64_t) * h->support_len; src = h->support; break;
+    case BICADMM_FIELD_TRACE:
+        for (auto& row : h->trace) tmp.insert(tmp.end(), row.begin(), row.end());
+        sz = sizeof(double) * tmp.size(); src = tmp.data(); host_src = true;
+        break;
+    case BICADMM_FIELD_INNER_COUNTS:
+        sz = sizeof(int32_t) * h->inner_counts.size(); src = h->inner_counts.data(); host_src = true;
+        break;
+    case BICADMM_FIELD_LAUNCHES: {
+        static thread_local int64_t nl;
+        nl = g_launches.load() - h->launches0;
+        sz = sizeof(int64_t); src = &nl; host_src = true;
+        break;
+    }
+    case BICADMM_FIELD_PHASE_MS:
+        tmp.assign(h->phase_ms, h->phase_ms + BICADMM_NPHASE);
+        sz = sizeof(double) * BICADMM_NPHASE; src = tmp.data(); host_src = true;
+        break;
+    case BICADMM_FIELD_PHASE_COUNT:
+        sz = sizeof(int64_t) * BICADMM_NPHASE; src = h->phase_cnt; host_src = true;
+        break;
+    default: return fail(h, BICADMM_ERR_INVALID, "unknown field");
+    }
+    if (bytes_out) *bytes_out = sz;
+    if (!dst) return BICADMM_OK;
+    if (bytes != sz) return fail(h, BICADMM_ERR_DIM, "bytes must equal the field size");
+    if (sz == 0) return BICADMM_OK;
+    if (h->dead) return BICADMM_ERR_STATE;
+    const cudaMemcpyKind kind = host_src ? (on_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost)
+                                         : (on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    if (!pieces.empty()) {
+        size_t off = 0;
+        for (size_t k = 0; k < pieces.size(); ++k) {
+            H_CUDA(h, cudaMemcpyAsync((char*)dst + off, pieces[k], piece_sz[k],
+                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+            off += piece_sz[k];
+        }
+    } else {
+        H_CUDA(h, cudaMemcpyAsync(dst, src, sz, kind, h->st));
+    }
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    return BICADMM_OK;
+}
+
+extern "C" int bicadmm_set_profiling(bicadmm_handle* h, int on) {
+    if (!h) return BICADMM_ERR_INVALID;
+    if (h->dead) return BICADMM_ERR_STATE;
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    resolve_phases(h);
+    for (int k = 0; k < BICADMM_NPHASE; ++k) { h->phase_ms[k] = 0.0; h->phase_cnt[k] = 0; }
+    h->prof = on != 0;
+    return BICADMM_OK;
+}
+
+extern "C" const char* bicadmm_last_error(const bicadmm_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+extern "C" int bicadmm_destroy(bicadmm_handle* h) {
+    if (!h) return BICADMM_OK;
+    if (h->st || true) cudaStreamSynchronize(h->st);
+    if (h->host_sc) cudaFreeHost(h->host_sc);
+    if (h->host_i64) cudaFreeHost(h->host_i64);
+    if (h->e0) cudaEventDestroy(h->e0);
+    if (h->e1) cudaEventDestroy(h->e1);
+    for (auto e : h->evpool) cudaEventDestroy(e);
+    delete h;
+    return BICADMM_OK;
+}

@@ -1,0 +1,290 @@
+// k_factor.cu -- one-time block factor of the x-update.
+//
+// Eq. (24)'s x_ij-step is the ridge least-squares problem whose normal equations
+// (DESIGN R17) are  (rho_l A_ij^T A_ij + c I) x = rho_l A_ij^T q + rho_c (z_j - u_ij),
+// c = 1/(N gamma) + rho_c.  We build H_ij = F^{-1} explicitly once, so every sweep's
+// solve is one more HBM-streamed GEMV (a3) instead of two latency-bound
+// triangular solves:
+//   G = A^T A                       (FP64 tensor-core DMMA tiles, SASS DMMA.8x8x4)
+//   F = rho_l G + c I;  F = L L^T   (right-looking blocked Cholesky, nb = 64)
+//   W = L^{-1}                      (blocked forward substitution, GEMM-shaped)
+//   H = W^T W                       (DMMA, triangular K range, mirrored)
+// FP64 tensor cores exist on sm_100a only as mma.sync DMMA; tcgen05 has no f64
+// kind.  In FP32 mode the factor is still built in FP64 and H rounded once.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bic {
+
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+constexpr int kGemmThreads = 128;
+
+struct GemmArgs {
+    int64_t M, N, K;
+    double alpha, beta, diag;
+    const void* A; int64_t lda;
+    const void* B; int64_t ldb;
+    void* C; int64_t ldc;
+    int lower_only;   // skip tiles strictly above the diagonal
+    int mirror;       // also write the transpose into the upper triangle
+    int tri_k;        // K range starts at max(m0, n0) (lower-triangular operands)
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// A(i, k): A_KFAST -> A[i*lda + k] (stored M x K), else A[k*lda + i] (stored K x M)
+// B(k, j): B_KFAST -> B[j*ldb + k] (stored N x K), else B[k*ldb + j] (stored K x N)
+template <typename TIN, typename TOUT, bool A_KFAST, bool B_KFAST>
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_dmma(const GemmArgs g) {
+    __shared__ double As[2][BK][BM + PAD];
+    __shared__ double Bs[2][BK][BN + PAD];
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (g.lower_only && n0 > m0 + BM - 1) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int grp = lane >> 2, tig = lane & 3;
+    const TIN* A = static_cast<const TIN*>(g.A);
+    const TIN* B = static_cast<const TIN*>(g.B);
+
+    int64_t kb = 0;
+    if (g.tri_k) kb = (m0 > n0 ? m0 : n0) / BK * BK;
+    const int64_t K = g.K;
+
+    double regA[8], regB[8];
+    auto gload = [&](int64_t k0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = tid + kGemmThreads * e;
+            int ii, kk;
+            if (A_KFAST) { ii = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; ii = idx & 63; }
+            const int64_t gi = m0 + ii, gk = k0 + kk;
+            double v = 0.0;
+            if (gi < g.M && gk < K) v = (double)(A_KFAST ? A[gi * g.lda + gk] : A[gk * g.lda + gi]);
+            regA[e] = v;
+            int jj;
+            if (B_KFAST) { jj = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; jj = idx & 63; }
+            const int64_t gj = n0 + jj, gk2 = k0 + kk;
+            double w = 0.0;
+            if (gj < g.N && gk2 < K) w = (double)(B_KFAST ? B[gj * g.ldb + gk2] : B[gk2 * g.ldb + gj]);
+            regB[e] = w;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int idx = tid + kGemmThreads * e;
+            int ii, kk;
+            if (A_KFAST) { ii = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; ii = idx & 63; }
+            As[buf][kk][ii] = regA[e];
+            int jj;
+            if (B_KFAST) { jj = idx >> 4; kk = idx & 15; } else { kk = idx >> 6; jj = idx & 63; }
+            Bs[buf][kk][jj] = regB[e];
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    if (kb < K) {
+        gload(kb);
+        sstore(0);
+        __syncthreads();
+        int buf = 0;
+        for (int64_t k0 = kb; k0 < K; k0 += BK) {
+            const bool more = k0 + BK < K;
+            if (more) gload(k0 + BK);
+#pragma unroll
+            for (int ks = 0; ks < BK; ks += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    af[t] = As[buf][ks + tig][wm * 32 + t * 8 + grp];
+                    bf[t] = Bs[buf][ks + tig][wn * 32 + t * 8 + grp];
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            }
+            if (more) {
+                sstore(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    }
+    TOUT* C = static_cast<TOUT*>(g.C);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t i = m0 + wm * 32 + a * 8 + grp;
+                const int64_t j = n0 + wn * 32 + b * 8 + tig * 2 + h;
+                if (i >= g.M || j >= g.N) continue;
+                double v = g.alpha * acc[a][b][h];
+                if (g.beta != 0.0) v += g.beta * (double)C[i * g.ldc + j];
+                if (i == j) v += g.diag;
+                C[i * g.ldc + j] = (TOUT)v;
+                if (g.mirror && i > j) C[j * g.ldc + i] = (TOUT)v;
+            }
+}
+
+template <typename TIN, typename TOUT, bool AK, bool BK_>
+static int gemm(const GemmArgs& g, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0) return BICADMM_OK;
+    dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
+    k_gemm_dmma<TIN, TOUT, AK, BK_><<<grid, kGemmThreads, 0, s>>>(g);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag,
+                double* G, int64_t ldg, bool full, cudaStream_t s) {
+    GemmArgs g{};
+    g.M = nj; g.N = nj; g.K = m;
+    g.alpha = alpha; g.beta = 0.0; g.diag = diag;
+    g.A = A; g.lda = lda; g.B = A; g.ldb = lda; g.C = G; g.ldc = ldg;
+    g.lower_only = 1; g.mirror = full ? 1 : 0; g.tri_k = 0;
+    // A^T A: A(i,k) = A[k*lda + i] (stored K x M), B(k,j) = A[k*lda + j] (stored K x N)
+    if (dtype == BICADMM_F64) return gemm<double, double, false, false>(g, s);
+    return gemm<float, double, false, false>(g, s);
+}
+
+// ------------------------------------------------------------------ Cholesky diag block
+// One CTA factors the kn x kn diagonal block (kn <= 64) of F in place (lower, upper
+// zeroed) and writes W_kk = L_kk^{-1} (lower) into Wd.  Unblocked right-looking
+// Cholesky in shared memory, then column-parallel forward substitution.
+constexpr int NB = 64;
+constexpr int kDiagThreads = 256;
+
+__global__ void __launch_bounds__(kDiagThreads) k_chol_diag(double* F, int64_t ldf, double* Wd, int64_t ldw, int kn,
+                                                          int* info) {
+    extern __shared__ double sm[];
+    double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(sm);
+    double (*W)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(sm + NB * (NB + 1));
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kn * kn; e += kDiagThreads) {
+        const int i = e / kn, j = e % kn;
+        L[i][j] = j <= i ? F[i * ldf + j] : 0.0;
+        W[i][j] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < kn; ++j) {
+        if (tid == 0) {
+            const double d = L[j][j];
+            if (!(d > 0.0)) { atomicExch(info, 1); L[j][j] = 1.0; }
+            else L[j][j] = sqrt(d);
+        }
+        __syncthreads();
+        const double ljj = L[j][j];
+        for (int i = j + 1 + tid; i < kn; i += kDiagThreads) L[i][j] /= ljj;
+        __syncthreads();
+        const int rem = kn - j - 1;
+        for (int e = tid; e < rem * rem; e += kDiagThreads) {
+            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+        }
+        __syncthreads();
+    }
+    if (tid < kn) {
+        const int c = tid;
+        W[c][c] = 1.0 / L[c][c];
+        for (int i = c + 1; i < kn; ++i) {
+            double s = 0.0;
+            for (int k = c; k < i; ++k) s += L[i][k] * W[k][c];
+            W[i][c] = -s / L[i][i];
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < kn * kn; e += kDiagThreads) {
+        const int i = e / kn, j = e % kn;
+        F[i * ldf + j] = j <= i ? L[i][j] : 0.0;
+        Wd[i * ldw + j] = W[i][j];
+    }
+}
+
+static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+size_t factor_ws_doubles(int64_t nj) {
+    const int64_t ld = round_up(nj, 8);
+    return (size_t)(ld * nj + NB * ld + 8);
+}
+
+int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype, double* ws,
+                   cudaStream_t s) {
+    const int64_t ldw = round_up(nj, 8);
+    double* W = ws;                 // nj x ldw, lower triangular L^{-1}
+    double* X = ws + ldw * nj;      // NB x ldw scratch
+    int* info = reinterpret_cast<int*>(X + NB * ldw);
+    BIC_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)(ldw * nj), s));
+    BIC_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
+    const size_t diag_smem = sizeof(double) * 2 * NB * (NB + 1);
+    static bool attr_set = false;
+    if (!attr_set) {
+        BIC_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem));
+        attr_set = true;
+    }
+    const int64_t nblk = (nj + NB - 1) / NB;
+    // right-looking blocked Cholesky of F (lower triangle of G)
+    for (int64_t kbk = 0; kbk < nblk; ++kbk) {
+        const int64_t k0 = kbk * NB, kn = nj - k0 < NB ? nj - k0 : NB, rest = nj - k0 - kn;
+        k_chol_diag<<<1, kDiagThreads, diag_smem, s>>>(G + k0 * ldg + k0, ldg, W + k0 * ldw + k0, ldw, (int)kn, info);
+        BIC_LAUNCHED();
+        if (rest <= 0) break;
+        double* F21 = G + (k0 + kn) * ldg + k0;
+        {   // panel: L21 = F21 W_kk^T  (in place; one tile column, all K read before write)
+            GemmArgs g{};
+            g.M = rest; g.N = kn; g.K = kn; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+            g.A = F21; g.lda = ldg; g.B = W + k0 * ldw + k0; g.ldb = ldw; g.C = F21; g.ldc = ldg;
+            int rc = gemm<double, double, true, true>(g, s);
+            if (rc) return rc;
+        }
+        {   // trailing: F22 -= L21 L21^T (lower tiles)
+            GemmArgs g{};
+            g.M = rest; g.N = rest; g.K = kn; g.alpha = -1.0; g.beta = 1.0; g.diag = 0.0;
+            g.A = F21; g.lda = ldg; g.B = F21; g.ldb = ldg;
+            g.C = G + (k0 + kn) * ldg + (k0 + kn); g.ldc = ldg; g.lower_only = 1;
+            int rc = gemm<double, double, true, true>(g, s);
+            if (rc) return rc;
+        }
+    }
+    // W = L^{-1}: block row i:  W_i,<i = -W_ii (L_i,<i W_<i,<i)
+    for (int64_t ib = 1; ib < nblk; ++ib) {
+        const int64_t i0 = ib * NB, in = nj - i0 < NB ? nj - i0 : NB;
+        {
+            GemmArgs g{};
+            g.M = in; g.N = i0; g.K = i0; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+            g.A = G + i0 * ldg; g.lda = ldg; g.B = W; g.ldb = ldw; g.C = X; g.ldc = ldw;
+            int rc = gemm<double, double, true, false>(g, s);
+            if (rc) return rc;
+        }
+        {
+            GemmArgs g{};
+            g.M = in; g.N = i0; g.K = in; g.alpha = -1.0; g.beta = 0.0; g.diag = 0.0;
+            g.A = W + i0 * ldw + i0; g.lda = ldw; g.B = X; g.ldb = ldw; g.C = W + i0 * ldw; g.ldc = ldw;
+            int rc = gemm<double, double, true, false>(g, s);
+            if (rc) return rc;
+        }
+    }
+    // H = W^T W  (W lower: K range from max(m0, n0)); lower tiles mirrored
+    GemmArgs g{};
+    g.M = nj; g.N = nj; g.K = nj; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+    g.A = W; g.lda = ldw; g.B = W; g.ldb = ldw; g.C = H; g.ldc = ldh;
+    g.lower_only = 1; g.mirror = 1; g.tri_k = 1;
+    int rc = dtype == BICADMM_F64 ? gemm<double, double, false, false>(g, s) : gemm<double, float, false, false>(g, s);
+    if (rc) return rc;
+    int hinfo = 0;
+    BIC_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BIC_CUDA(cudaStreamSynchronize(s));
+    return hinfo ? BICADMM_ERR_INVALID : BICADMM_OK;
+}
+
+}  // namespace bic

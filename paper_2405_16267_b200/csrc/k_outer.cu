@@ -1,0 +1,406 @@
+// k_outer.cu -- the global (consensus) step of Bi-cADMM, replicated on every rank
+// (Algorithm 1 "Global Updates").
+//
+//   Collect  : wbar = (1/N) sum_i (x_i + u_i)                       (DESIGN R1)
+//   (7b)     : (z, t) = argmin_{||z||_1 <= t} (N rho_c/2)||z - wbar||^2 + (rho_b/2)(s'z - t + v)^2
+//              exact: z_l = sgn(w_l) max(|w_l| - tau d_l, 0), d_l = 1 - s_l sgn(w_l),
+//              tau the root of N rho_c tau = rho_b (psi(tau) - v), psi(tau) = sum d_l |z_l(tau)|
+//              (DESIGN R3).  Root: 16-way multisection on the IEEE bit
+//              patterns of tau to isolate the active set, then the exact segment formula.
+//   (13)     : s = clamp((t - v)/Mcap, -1, 1) sgn(z) 1_T, T = top-kappa |z| (ties -> lower
+//              index; DESIGN R4).  Device radix select on the uint64 bit patterns of |z|.
+//   (14)     : g = z's - t, v += g                                  (DESIGN R5)
+//   (9)      : u_ij += x_ij - z_j
+//   (15)     : p_r = sum_i ||x_i - z||, d_r = sqrt(N) rho_c ||z - z_prev||, b_r = |g|
+// The global step is O(n) and latency-bound; it runs in single-CTA kernels with
+// fixed-order block reductions so every rank computes bit-identical z, s, v.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bic {
+
+constexpr int kOuterThreads = 1024;
+constexpr int kProbes = 15;  // interior probes per multisection pass (16-way)
+
+__device__ __forceinline__ uint64_t dkey(double a) { return (uint64_t)__double_as_longlong(a); }
+__device__ __forceinline__ double kdbl(uint64_t k) { return __longlong_as_double((long long)k); }
+
+// ------------------------------------------------------------------ (7b)
+__global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double rho_c, double rho_b,
+                                                     const double* __restrict__ wsum, const double* __restrict__ s,
+                                                     double* __restrict__ wbar, double* __restrict__ z,
+                                                     double* __restrict__ z_prev, OuterScalars* sc) {
+    __shared__ double scratch[32];
+    __shared__ double probe_red[32][kProbes + 1];
+    __shared__ uint64_t s_lo, s_hi;
+    const double v = sc->v;
+    const double Nd = (double)N, Nrc = Nd * rho_c;
+    double psi0 = 0.0, sw = 0.0, bmax = 0.0;
+    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+        const double w = wsum[l] / Nd;
+        wbar[l] = w;
+        z_prev[l] = z[l];
+        const double d = 1.0 - s[l] * sgn(w);
+        psi0 += d * fabs(w);
+        sw += s[l] * w;
+        if (d > 0.0 && w != 0.0) bmax = fmax(bmax, fabs(w) / d);
+    }
+    psi0 = block_sum(psi0, scratch);
+    sw = block_sum(sw, scratch);
+    bmax = block_max(bmax, scratch);
+
+    double tau = 0.0;
+    const bool case1 = psi0 <= v;
+    if (!case1) {
+        // f(tau) = N rho_c tau - rho_b (psi(tau) - v): increasing; f(0) < 0.
+        // f(bmax) = N rho_c bmax + rho_b v (psi(bmax) = 0).
+        double Asum, Bsum;
+        if (Nrc * bmax + rho_b * v <= 0.0) {
+            Asum = 0.0; Bsum = 0.0;   // every shrinkable coordinate is zero
+        } else {
+            if (threadIdx.x == 0) { s_lo = 0; s_hi = dkey(bmax); }
+            __syncthreads();
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            for (int pass = 0; pass < 40; ++pass) {
+                const uint64_t lo = s_lo, hi = s_hi;
+                if (hi - lo <= 1) break;
+                const uint64_t d = hi - lo;
+                double tp[kProbes], acc[kProbes];
+#pragma unroll
+                for (int p = 0; p < kProbes; ++p) {
+                    const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
+                    tp[p] = kdbl(kp);
+                    acc[p] = 0.0;
+                }
+                for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+                    const double w = wbar[l];
+                    const double dl = 1.0 - s[l] * sgn(w);
+                    if (dl > 0.0) {
+                        const double aw = fabs(w);
+#pragma unroll
+                        for (int p = 0; p < kProbes; ++p) acc[p] += dl * fmax(aw - tp[p] * dl, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < kProbes; ++p) {
+                    const double t = warp_sum(acc[p]);
+                    if (lane == 0) probe_red[wid][p] = t;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    int best = -1;  // largest probe with f <= 0
+                    for (int p = 0; p < kProbes; ++p) {
+                        double psi = 0.0;
+                        for (int ww = 0; ww < kOuterThreads / 32; ++ww) psi += probe_red[ww][p];
+                        const double f = Nrc * tp[p] - rho_b * (psi - v);
+                        if (f <= 0.0) best = p;
+                    }
+                    uint64_t nlo = lo, nhi = hi;
+                    for (int p = 0; p < kProbes; ++p) {
+                        const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
+                        if (p <= best) nlo = kp;
+                        else if (kp < nhi && kp > nlo) { nhi = kp; break; }
+                    }
+                    s_lo = nlo; s_hi = nhi;
+                }
+                __syncthreads();
+            }
+            const double tlo = kdbl(s_lo);
+            double a = 0.0, b = 0.0;
+            for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+                const double w = wbar[l];
+                const double dl = 1.0 - s[l] * sgn(w);
+                if (dl > 0.0 && w != 0.0 && fabs(w) / dl > tlo) { a += dl * fabs(w); b += dl * dl; }
+            }
+            Asum = block_sum(a, scratch);
+            Bsum = block_sum(b, scratch);
+        }
+        tau = rho_b * (Asum - v) / (Nrc + rho_b * Bsum);
+    }
+    double l1 = 0.0, dz2 = 0.0;
+    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+        const double w = wbar[l];
+        double zl;
+        if (case1) zl = w;
+        else {
+            const double dl = 1.0 - s[l] * sgn(w);
+            zl = sgn(w) * fmax(fabs(w) - tau * dl, 0.0);
+        }
+        z[l] = zl;
+        l1 += fabs(zl);
+        const double e = zl - z_prev[l];
+        dz2 += e * e;
+    }
+    l1 = block_sum(l1, scratch);
+    dz2 = block_sum(dz2, scratch);
+    if (threadIdx.x == 0) {
+        sc->t = case1 ? sw + v : l1;
+        sc->tau = tau;
+        sc->dz2 = dz2;
+        sc->psi0 = psi0;
+    }
+}
+
+int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s, double* wbar,
+              double* z, double* z_prev, OuterScalars* sc, cudaStream_t st) {
+    k_zt<<<1, kOuterThreads, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// ------------------------------------------------------------------ top-kappa selection
+// Radix select (8 passes x 8 bits, MSB first) of the kk-th largest key among keys
+// of |z|; returns threshold key K and the number `take` of elements with key == K
+// that belong to T (lowest indices first).  If nonzero_only, zero keys never count.
+struct TopK { uint64_t K; int64_t take; int64_t kk; };
+
+__device__ TopK radix_topk(int64_t len, int64_t kk, const double* __restrict__ z, bool nonzero_only) {
+    __shared__ int hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ int64_t s_rem, s_nz;
+    TopK r;
+    if (nonzero_only) {
+        int cnt = 0;
+        for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) cnt += z[l] != 0.0;
+        if (threadIdx.x == 0) s_nz = 0;
+        __syncthreads();
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_nz), (unsigned long long)cnt);
+        __syncthreads();
+        if (kk > s_nz) kk = s_nz;
+    }
+    r.kk = kk;
+    if (kk <= 0) { r.K = ~0ull; r.take = 0; return r; }
+    if (threadIdx.x == 0) { s_prefix = 0; s_rem = kk; }
+    __syncthreads();
+    uint64_t mask = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int b = threadIdx.x; b < 256; b += kOuterThreads) hist[b] = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+        for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+            const uint64_t key = dkey(fabs(z[l]));
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t rem = s_rem, cum = 0;
+            int sel = 0;
+            for (int b = 255; b >= 0; --b) {
+                if (cum + hist[b] >= rem) { sel = b; rem -= cum; break; }
+                cum += hist[b];
+            }
+            s_prefix = prefix | ((uint64_t)sel << shift);
+            s_rem = rem;
+        }
+        mask |= (uint64_t)255 << shift;
+        __syncthreads();
+    }
+    r.K = s_prefix;
+    r.take = s_rem;
+    __syncthreads();
+    return r;
+}
+
+// Visit elements of T in ascending index order, contiguous range per thread.
+// f(l, rank_in_T_for_this_thread_ordering) is called for members.
+template <typename F>
+__device__ void for_members(int64_t len, const double* __restrict__ z, const TopK& tk, bool nonzero_only,
+                            int64_t* scan_scratch, F f) {
+    const int64_t per = (len + kOuterThreads - 1) / kOuterThreads;
+    const int64_t l0 = threadIdx.x * per, l1 = l0 + per < len ? l0 + per : len;
+    int64_t eq = 0, mem = 0;
+    for (int64_t l = l0; l < l1; ++l) {
+        const uint64_t key = dkey(fabs(z[l]));
+        if (nonzero_only && key == 0) continue;
+        if (key == tk.K) ++eq;
+    }
+    int64_t total;
+    const int64_t eq_before = block_exclusive_scan(eq, scan_scratch, &total);
+    // members in this thread's range = (#key > K) + min(max(take - eq_before, 0), eq)
+    for (int64_t l = l0; l < l1; ++l) {
+        const uint64_t key = dkey(fabs(z[l]));
+        if (nonzero_only && key == 0) continue;
+        if (key > tk.K && tk.kk > 0) ++mem;
+    }
+    int64_t take_here = tk.take - eq_before;
+    if (take_here < 0) take_here = 0;
+    if (take_here > eq) take_here = eq;
+    mem += take_here;
+    int64_t mem_total;
+    const int64_t mem_before = block_exclusive_scan(mem, scan_scratch, &mem_total);
+    int64_t seen_eq = 0, pos = mem_before;
+    for (int64_t l = l0; l < l1; ++l) {
+        const uint64_t key = dkey(fabs(z[l]));
+        if (nonzero_only && key == 0) continue;
+        bool in = false;
+        if (tk.kk > 0) {
+            if (key > tk.K) in = true;
+            else if (key == tk.K) { in = seen_eq < take_here; ++seen_eq; }
+        }
+        if (in) f(l, pos++);
+    }
+}
+
+__global__ void __launch_bounds__(kOuterThreads) k_s_update(int64_t len, int64_t kappa, const double* __restrict__ z,
+                                                           double* __restrict__ s, OuterScalars* sc) {
+    __shared__ double scratch[32];
+    __shared__ int64_t scan_scratch[32];
+    const double t = sc->t, v = sc->v;
+    const int64_t kk = kappa < len ? kappa : len;
+    const TopK tk = radix_topk(len, kk, z, false);
+    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) s[l] = 0.0;
+    __syncthreads();
+    double mc = 0.0;
+    for_members(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { mc += fabs(z[l]); });
+    const double mcap = block_sum(mc, scratch);
+    const double scale = mcap > 0.0 ? fmin(fmax((t - v) / mcap, -1.0), 1.0) : 0.0;
+    if (mcap > 0.0)
+        for_members(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { s[l] = scale * sgn(z[l]); });
+    __syncthreads();
+    double zs = 0.0;
+    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) zs += z[l] * s[l];
+    zs = block_sum(zs, scratch);
+    if (threadIdx.x == 0) {
+        const double g = zs - t;
+        sc->mcap = mcap;
+        sc->g = g;
+        sc->v = v + g;
+    }
+}
+
+int launch_s_update(int64_t len, int64_t kappa, const double* z, double* s, OuterScalars* sc, cudaStream_t st) {
+    k_s_update<<<1, kOuterThreads, 0, st>>>(len, kappa, z, s, sc);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+__global__ void __launch_bounds__(kOuterThreads) k_support(int64_t len, int64_t kappa, const double* __restrict__ z,
+                                                          int64_t* __restrict__ support, int64_t* count) {
+    __shared__ int64_t scan_scratch[32];
+    const int64_t kk = kappa < len ? kappa : len;
+    const TopK tk = radix_topk(len, kk, z, true);
+    for_members(len, z, tk, true, scan_scratch, [&](int64_t l, int64_t pos) { support[pos] = l; });
+    if (threadIdx.x == 0) *count = tk.kk;
+}
+
+int launch_support(int64_t len, int64_t kappa, const double* z, int64_t* support, int64_t* count, cudaStream_t st) {
+    k_support<<<1, kOuterThreads, 0, st>>>(len, kappa, z, support, count);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// ------------------------------------------------------------------ Collect / (9) / (15)
+__global__ void k_wsum(int64_t len, int64_t stride, const double* __restrict__ x_all,
+                       const double* __restrict__ u_all, int nl, double* __restrict__ wsum) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= len) return;
+    double acc = 0.0;
+    for (int i = 0; i < nl; ++i) acc += x_all[(int64_t)i * stride + l] + u_all[(int64_t)i * stride + l];
+    wsum[l] = acc;
+}
+
+int launch_wsum(int64_t len, int64_t stride, const double* x_all, const double* u_all, int nl, double* wsum,
+                cudaStream_t s) {
+    k_wsum<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(len, stride, x_all, u_all, nl, wsum);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+struct UBatch {
+    BlockVec b[kMaxDesc];
+    int nb;
+};
+constexpr int kUPer = 4;  // elements per thread
+
+__global__ void __launch_bounds__(kUThreads) k_u_update(const __grid_constant__ UBatch B, const double* __restrict__ z,
+                                                        double* __restrict__ partial, int64_t partial_base) {
+    __shared__ double scratch[32];
+    const int64_t cta = blockIdx.x;
+    int bi = 0;
+    while (bi + 1 < B.nb && cta >= B.b[bi + 1].cta_begin) ++bi;
+    const BlockVec& V = B.b[bi];
+    const int64_t e0 = (cta - V.cta_begin) * (kUThreads * kUPer);
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < kUPer; ++k) {
+        const int64_t e = e0 + threadIdx.x + k * kUThreads;
+        if (e < V.len) {
+            const double x = V.x[e], zl = z[V.c0 + e];
+            const double d = x - zl;
+            V.u[e] += d;
+            sq += d * d;
+        }
+    }
+    sq = block_sum(sq, scratch);
+    if (threadIdx.x == 0) partial[partial_base + cta] = sq;
+}
+
+int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s) {
+    int64_t base = 0;
+    for (int b0 = 0; b0 < nb; b0 += kMaxDesc) {
+        UBatch B;
+        B.nb = nb - b0 < kMaxDesc ? nb - b0 : kMaxDesc;
+        int64_t t = 0;
+        for (int k = 0; k < B.nb; ++k) {
+            B.b[k] = bv[b0 + k];
+            B.b[k].cta_begin = t;
+            bv[b0 + k].cta_begin = base + t;   // record global partial offsets for node_sq
+            t += (B.b[k].len + kUThreads * kUPer - 1) / (kUThreads * kUPer);
+        }
+        if (t > 0) {
+            k_u_update<<<(unsigned)t, kUThreads, 0, s>>>(B, z, partial, base);
+            BIC_LAUNCHED();
+        }
+        base += t;
+    }
+    return BICADMM_OK;
+}
+
+struct NodeSqArgs {
+    int64_t begin[kMaxDesc * 4], count[kMaxDesc * 4];
+    int32_t node[kMaxDesc * 4];
+    int nb;
+};
+
+__global__ void k_node_sq(const __grid_constant__ NodeSqArgs A, const double* __restrict__ partial, int N,
+                          double* __restrict__ node_sq) {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < A.nb; ++b)
+            if (A.node[b] == i)
+                for (int64_t k = 0; k < A.count[b]; ++k) acc += partial[A.begin[b] + k];
+        node_sq[i] = acc;
+    }
+}
+
+int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq, cudaStream_t s) {
+    if (nb > kMaxDesc * 4) return BICADMM_ERR_PLACEMENT;
+    NodeSqArgs A;
+    A.nb = nb;
+    for (int b = 0; b < nb; ++b) {
+        A.begin[b] = bv[b].cta_begin;
+        A.count[b] = (bv[b].len + kUThreads * kUPer - 1) / (kUThreads * kUPer);
+        A.node[b] = bv[b].node;
+    }
+    k_node_sq<<<1, 64, 0, s>>>(A, partial, N, node_sq);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+__global__ void k_residuals(int N, double sqrtN_rho_c, const double* __restrict__ node_sq, OuterScalars* sc) {
+    if (threadIdx.x != 0) return;
+    double pr = 0.0;
+    for (int i = 0; i < N; ++i) pr += sqrt(node_sq[i]);
+    sc->p_r = pr;
+    sc->d_r = sqrtN_rho_c * sqrt(sc->dz2);
+    sc->b_r = fabs(sc->g);
+}
+
+int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s) {
+    k_residuals<<<1, 32, 0, s>>>(N, sqrtN_rho_c, node_sq, sc);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+}  // namespace bic

@@ -1,0 +1,280 @@
+// k_prox.cu -- per-sample loss prox and dual update of the node-level sharing
+// ADMM (Eqs. (22), (23)), fused with the q-vector
+// formation of the next sweep (a1, Eq. (24)).
+//
+// For node i and sample r (C classes for softmax):
+//   S     = sum_j A_ij x_ij            (block sum; P:244 AllReduce when blocks span GPUs)
+//   abar  = S / M
+//   omega = argmin_w phi(M w, b_r) + (M rho_l / 2) ||w - (abar + nu)||^2   (22)
+//   nu   += abar - omega               (23)
+//   delta = omega - abar - nu          (so q_ij = p_ij + delta, Eq. (24))
+// "the omega-update splits entirely into m_i scalar optimization problems":
+// one thread per sample.  LS and hinge are closed forms; logistic uses a
+// safeguarded Newton iteration (bracket [p - 1/rho_l, p + 1/rho_l]); softmax a
+// damped Newton step with the Sherman-Morrison inverse of M(diag pi - pi pi^T) + rho_l I.
+#include "common.cuh"
+#include "kernels.h"
+#include <cfloat>
+
+namespace bic {
+
+struct ProxBatch {
+    ProxNode n[kMaxDesc];
+    int nn;
+    int64_t total_ctas;
+};
+
+__device__ __forceinline__ double sigmoid(double a) {
+    if (a >= 0.0) return 1.0 / (1.0 + exp(-a));
+    const double e = exp(a);
+    return e / (1.0 + e);
+}
+
+__device__ __forceinline__ double prox_logistic(int M, double rho, double b, double p) {
+    // root of g(w) = -b sigma(-b M w) + rho (w - p), g' = M sigma (1 - sigma) + rho > 0
+    double lo = p - 1.0 / rho, hi = p + 1.0 / rho, w = p;
+    const double Md = (double)M;
+    for (int it = 0; it < 60; ++it) {
+        const double sg = sigmoid(-b * Md * w);
+        const double g = -b * sg + rho * (w - p);
+        if (g > 0.0) hi = w; else lo = w;
+        const double gp = Md * sg * (1.0 - sg) + rho;
+        double wn = w - g / gp;
+        if (!(wn > lo && wn < hi)) wn = 0.5 * (lo + hi);
+        const double step = fabs(wn - w);
+        w = wn;
+        if (step <= 4.0 * DBL_EPSILON * fmax(1.0, fabs(w))) break;
+    }
+    return w;
+}
+
+__device__ __forceinline__ double prox_hinge(int M, double rho, double b, double p) {
+    const double pp = b * p, Md = (double)M;
+    double y;
+    if (Md * pp > 1.0) y = pp;
+    else if (Md * (pp + 1.0 / rho) < 1.0) y = pp + 1.0 / rho;
+    else y = 1.0 / Md;
+    return b * y;
+}
+
+template <int CM>
+__device__ double softmax_obj(int C, double Md, double rho, int y, const double* p, const double* w) {
+    double mx = -INFINITY;
+    for (int c = 0; c < C; ++c) mx = fmax(mx, Md * w[c]);
+    double se = 0.0, q = 0.0;
+    for (int c = 0; c < C; ++c) { se += exp(Md * w[c] - mx); q += (w[c] - p[c]) * (w[c] - p[c]); }
+    return mx + log(se) - Md * w[y] + 0.5 * Md * rho * q;
+}
+
+template <int CM>
+__device__ void prox_softmax(int C, int M, double rho, int y, const double* p, double* w) {
+    const double Md = (double)M;
+    double pi[CM], g[CM], d[CM], tr[CM];
+    for (int c = 0; c < C; ++c) w[c] = p[c];
+    for (int it = 0; it < 100; ++it) {
+        double mx = -INFINITY;
+        for (int c = 0; c < C; ++c) mx = fmax(mx, Md * w[c]);
+        double se = 0.0;
+        for (int c = 0; c < C; ++c) { pi[c] = exp(Md * w[c] - mx); se += pi[c]; }
+        for (int c = 0; c < C; ++c) pi[c] /= se;
+        // H = D - M pi pi^T, D = rho + M pi  =>  H^{-1} g = D^{-1} g + M D^{-1} pi (pi^T D^{-1} g) / (1 - M pi^T D^{-1} pi)
+        double a = 0.0, bden = 0.0;
+        for (int c = 0; c < C; ++c) {
+            g[c] = pi[c] - (c == y ? 1.0 : 0.0) + rho * (w[c] - p[c]);
+            const double Dc = rho + Md * pi[c];
+            a += pi[c] * g[c] / Dc;
+            bden += pi[c] * pi[c] / Dc;
+        }
+        const double coef = Md * a / (1.0 - Md * bden);
+        double dmax = 0.0, wmax = 1.0;
+        for (int c = 0; c < C; ++c) d[c] = (g[c] + coef * pi[c]) / (rho + Md * pi[c]);
+        const double f0 = softmax_obj<CM>(C, Md, rho, y, p, w);
+        double step = 1.0;
+        for (int ls = 0; ls < 60; ++ls) {
+            for (int c = 0; c < C; ++c) tr[c] = w[c] - step * d[c];
+            if (softmax_obj<CM>(C, Md, rho, y, p, tr) <= f0 + 1e-12 * (1.0 + fabs(f0))) break;
+            step *= 0.5;
+        }
+        for (int c = 0; c < C; ++c) {
+            const double dc = step * d[c];
+            dmax = fmax(dmax, fabs(dc));
+            w[c] -= dc;
+            wmax = fmax(wmax, fabs(w[c]));
+        }
+        if (dmax <= 4.0 * DBL_EPSILON * wmax) break;
+    }
+}
+
+template <typename T, int LOSS, int CM>
+__global__ void __launch_bounds__(kProxThreads) k_prox(const __grid_constant__ ProxBatch B, int C, int M,
+                                                       double rho) {
+    __shared__ double scratch[32];
+    const int64_t cta = blockIdx.x;
+    int ni = 0;
+    while (ni + 1 < B.nn && cta >= B.n[ni + 1].cta_begin) ++ni;
+    const ProxNode& P = B.n[ni];
+    const int64_t r = (cta - P.cta_begin) * kProxThreads + threadIdx.x;
+    double sq = 0.0;
+    if (r < P.m) {
+        const double Md = (double)M;
+        const double bl = (double)static_cast<const T*>(P.b)[r];
+        double abar[CM], pa[CM], om[CM];
+        for (int c = 0; c < C; ++c) {
+            double S;
+            if (P.S) {
+                S = P.S[r * C + c];
+            } else {
+                S = 0.0;
+                for (int j = 0; j < P.np; ++j) S += P.p[j * P.pstride + r * C + c];
+            }
+            abar[c] = S / Md;
+            pa[c] = abar[c] + P.nu[r * C + c];
+        }
+        if constexpr (LOSS == BICADMM_LS) {
+            om[0] = (2.0 * bl + rho * pa[0]) / (2.0 * Md + rho);
+        } else if constexpr (LOSS == BICADMM_LOGISTIC) {
+            om[0] = prox_logistic(M, rho, bl, pa[0]);
+        } else if constexpr (LOSS == BICADMM_HINGE) {
+            om[0] = prox_hinge(M, rho, bl, pa[0]);
+        } else {
+            prox_softmax<CM>(C, M, rho, (int)bl, pa, om);
+        }
+        for (int c = 0; c < C; ++c) {
+            const double nu = P.nu[r * C + c] + abar[c] - om[c];
+            P.nu[r * C + c] = nu;
+            P.delta[r * C + c] = om[c] - abar[c] - nu;
+            if (P.omega) P.omega[r * C + c] = om[c];
+            const double e = abar[c] - om[c];
+            sq += e * e;
+        }
+    }
+    if (P.sq_partial) {
+        const double s = block_sum(sq, scratch);
+        if (threadIdx.x == 0) P.sq_partial[cta - P.cta_begin] = s;
+    }
+}
+
+int launch_prox(int loss, int dtype, int C, int M, double rho_l, ProxNode* nodes, int nn, cudaStream_t s) {
+    if (C > 16 || (loss == BICADMM_SOFTMAX) != (C > 1)) return BICADMM_ERR_INVALID;
+    for (int base = 0; base < nn; base += kMaxDesc) {
+        ProxBatch B;
+        B.nn = nn - base < kMaxDesc ? nn - base : kMaxDesc;
+        int64_t t = 0;
+        for (int k = 0; k < B.nn; ++k) {
+            B.n[k] = nodes[base + k];
+            B.n[k].cta_begin = t;
+            t += (B.n[k].m + kProxThreads - 1) / kProxThreads;
+        }
+        B.total_ctas = t;
+        if (t == 0) continue;
+        const unsigned g = (unsigned)t;
+#define BIC_PROX(T)                                                                              \
+    switch (loss) {                                                                              \
+    case BICADMM_LS: k_prox<T, BICADMM_LS, 1><<<g, kProxThreads, 0, s>>>(B, C, M, rho_l); break; \
+    case BICADMM_LOGISTIC: k_prox<T, BICADMM_LOGISTIC, 1><<<g, kProxThreads, 0, s>>>(B, C, M, rho_l); break; \
+    case BICADMM_HINGE: k_prox<T, BICADMM_HINGE, 1><<<g, kProxThreads, 0, s>>>(B, C, M, rho_l); break; \
+    default: k_prox<T, BICADMM_SOFTMAX, 16><<<g, kProxThreads, 0, s>>>(B, C, M, rho_l); break; \
+    }
+        if (dtype == BICADMM_F64) { BIC_PROX(double) } else { BIC_PROX(float) }
+#undef BIC_PROX
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
+// Objective (1) data term: per-CTA partial sums of phi((sum_j p_j)[r], b_r)
+// into sq_partial (fixed-order block sums).
+template <typename T, int LOSS, int CM>
+__global__ void __launch_bounds__(kProxThreads) k_loss(const __grid_constant__ ProxBatch B, int C) {
+    __shared__ double scratch[32];
+    const int64_t cta = blockIdx.x;
+    int ni = 0;
+    while (ni + 1 < B.nn && cta >= B.n[ni + 1].cta_begin) ++ni;
+    const ProxNode& P = B.n[ni];
+    const int64_t r = (cta - P.cta_begin) * kProxThreads + threadIdx.x;
+    double f = 0.0;
+    if (r < P.m) {
+        const double bl = (double)static_cast<const T*>(P.b)[r];
+        double w[CM];
+        for (int c = 0; c < C; ++c) {
+            double S = 0.0;
+            if (P.S) S = P.S[r * C + c];
+            else for (int j = 0; j < P.np; ++j) S += P.p[j * P.pstride + r * C + c];
+            w[c] = S;
+        }
+        if constexpr (LOSS == BICADMM_LS) { const double e = w[0] - bl; f = e * e; }
+        else if constexpr (LOSS == BICADMM_LOGISTIC) {
+            const double a = -bl * w[0];
+            f = a > 0.0 ? a + log1p(exp(-a)) : log1p(exp(a));
+        } else if constexpr (LOSS == BICADMM_HINGE) { f = fmax(0.0, 1.0 - bl * w[0]); }
+        else {
+            double mx = -INFINITY, se = 0.0;
+            for (int c = 0; c < C; ++c) mx = fmax(mx, w[c]);
+            for (int c = 0; c < C; ++c) se += exp(w[c] - mx);
+            f = mx + log(se) - w[(int)bl];
+        }
+    }
+    const double s = block_sum(f, scratch);
+    if (threadIdx.x == 0) P.sq_partial[cta - P.cta_begin] = s;
+}
+
+int launch_loss(int loss, int dtype, int C, ProxNode* nodes, int nn, cudaStream_t s) {
+    for (int base = 0; base < nn; base += kMaxDesc) {
+        ProxBatch B;
+        B.nn = nn - base < kMaxDesc ? nn - base : kMaxDesc;
+        int64_t t = 0;
+        for (int k = 0; k < B.nn; ++k) {
+            B.n[k] = nodes[base + k];
+            B.n[k].cta_begin = t;
+            t += (B.n[k].m + kProxThreads - 1) / kProxThreads;
+        }
+        if (t == 0) continue;
+        const unsigned g = (unsigned)t;
+#define BIC_LOSS(T)                                                                          \
+    switch (loss) {                                                                          \
+    case BICADMM_LS: k_loss<T, BICADMM_LS, 1><<<g, kProxThreads, 0, s>>>(B, C); break;       \
+    case BICADMM_LOGISTIC: k_loss<T, BICADMM_LOGISTIC, 1><<<g, kProxThreads, 0, s>>>(B, C); break; \
+    case BICADMM_HINGE: k_loss<T, BICADMM_HINGE, 1><<<g, kProxThreads, 0, s>>>(B, C); break; \
+    default: k_loss<T, BICADMM_SOFTMAX, 16><<<g, kProxThreads, 0, s>>>(B, C); break;          \
+    }
+        if (dtype == BICADMM_F64) { BIC_LOSS(double) } else { BIC_LOSS(float) }
+#undef BIC_LOSS
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
+// S_out[k][r] = sum over the node's local blocks (ascending) of p  -- the local
+// contribution handed to the cross-GPU AllReduce (Algorithm 2).
+__global__ void __launch_bounds__(256) k_psum(const __grid_constant__ ProxBatch B, double* const* S_out_dev_unused,
+                                              int C) {
+    (void)S_out_dev_unused;
+    const int64_t cta = blockIdx.x;
+    int ni = 0;
+    while (ni + 1 < B.nn && cta >= B.n[ni + 1].cta_begin) ++ni;
+    const ProxNode& P = B.n[ni];
+    const int64_t e = (cta - P.cta_begin) * 256 + threadIdx.x;
+    if (e >= P.m * C) return;
+    double S = 0.0;
+    for (int j = 0; j < P.np; ++j) S += P.p[j * P.pstride + e];
+    const_cast<double*>(P.S)[e] = S;
+}
+
+int launch_psum(int C, ProxNode* nodes, int nn, double* const* /*S_out*/, cudaStream_t s) {
+    for (int base = 0; base < nn; base += kMaxDesc) {
+        ProxBatch B;
+        B.nn = nn - base < kMaxDesc ? nn - base : kMaxDesc;
+        int64_t t = 0;
+        for (int k = 0; k < B.nn; ++k) {
+            B.n[k] = nodes[base + k];
+            B.n[k].cta_begin = t;
+            t += (B.n[k].m * C + 255) / 256;
+        }
+        if (t == 0) continue;
+        k_psum<<<(unsigned)t, 256, 0, s>>>(B, nullptr, C);
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
+}  // namespace bic

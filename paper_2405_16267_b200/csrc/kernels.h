@@ -1,0 +1,102 @@
+// kernels.h -- private launcher declarations of libbicadmm (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace bic {
+
+// ---------------------------------------------------------------- GEMV family
+// y[r] = sum_l A[r, l] x[l]   ("Compute A_ij x_ij"; also x = H r, a3)
+struct GemvDesc {
+    const void* A;
+    int64_t lda, rows, cols;
+    const double* x;
+    double* y;
+    int64_t task_begin;  // filled by the launcher
+};
+int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s);
+int gemv_grid_cap(int dtype, int sm_count);  // persistent grid size (resident CTAs)
+
+// r[l] = rho_l * sum_r A[r, l] (p[r] + delta[r]) + rho_c (z[l] - u[l])   (Eq. (24))
+struct GemvTDesc {
+    const void* A;
+    int64_t lda, rows, cols;
+    const double* p;      // A_ij x_ij from the previous sweep
+    const double* delta;  // omega_bar - abar - nu of the node (may be null)
+    const double* z;      // z_j (may be null)
+    const double* u;      // u_ij (may be null)
+    double* r;            // output
+    double* partial;      // [nchunks][cols] scratch
+    int64_t chunk_rows;
+    int32_t nchunks, nstrips;
+    int64_t cta_begin;    // filled by the launcher
+};
+// Choose chunk_rows / nchunks for a batch so the grid fills the GPU; returns
+// scratch doubles needed by descriptor k in need[k].
+void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need);
+int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s,
+                  cudaEvent_t mid = nullptr);
+int gemv_t_strip_width(int dtype);
+
+// ---------------------------------------------------------------- prox (Eqs. (22), (23))
+struct ProxNode {
+    const void* b;        // labels (dtype)
+    const double* p;      // local block products, np blocks x pstride
+    const double* S;      // if non-null: the (all-reduced) block sum, used instead of p
+    double* nu;
+    double* delta;
+    double* omega;        // optional output
+    double* sq_partial;   // optional: per-CTA partial of ||abar - omega||^2 (tol mode)
+    int64_t m, pstride;
+    int32_t np;
+    int64_t cta_begin;    // filled by the launcher
+};
+int launch_prox(int loss, int dtype, int C, int M, double rho_l, ProxNode* nodes, int nn, cudaStream_t s);
+int launch_psum(int C, ProxNode* nodes, int nn, double* const* S_out, cudaStream_t s);
+constexpr int kProxThreads = 256;
+// Per-CTA partials of sum_r phi((sum_j p_j)[r], b_r) for the objective (DESIGN R20).
+int launch_loss(int loss, int dtype, int C, ProxNode* nodes, int nn, cudaStream_t s);
+
+// ---------------------------------------------------------------- dense factor (a0)
+// F = alpha A^T A + diag I (lower triangle or full) into FP64 G (ldg).
+int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
+                double diag, double* G, int64_t ldg, bool full, cudaStream_t s);
+// In-place: G (nj x nj FP64, lower triangle holding F) -> H = F^{-1} written to H (dtype, ldh).
+// ws: FP64 scratch of factor_ws_doubles(nj) doubles.
+size_t factor_ws_doubles(int64_t nj);
+int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype,
+                   double* ws, cudaStream_t s);
+
+// ---------------------------------------------------------------- outer step (a8-a12)
+struct OuterScalars {   // device-resident scalars of the global step
+    double t, v, tau, g, mcap, dz2, psi0, pad0;
+    double p_r, d_r, b_r, pad1;
+};
+int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s,
+              double* wbar, double* z, double* z_prev, OuterScalars* sc, cudaStream_t st);
+int launch_s_update(int64_t len, int64_t kappa, const double* z, double* s, OuterScalars* sc,
+                    cudaStream_t st);
+int launch_support(int64_t len, int64_t kappa, const double* z, int64_t* support, int64_t* count,
+                   cudaStream_t st);
+
+struct BlockVec {       // one local block's slice of the n*C vectors
+    double* x;          // x_ij (n_j*C)
+    double* u;          // u_ij
+    int64_t c0, len;    // offset into the global n*C vector, length n_j*C
+    int32_t node;       // global node id
+    int64_t cta_begin;  // filled by the launcher
+};
+// wsum[l] = sum over local nodes (ascending) of x_i[l] + u_i[l]  ("Collect");
+// x_all / u_all hold one full-length n*C vector per local node (zero off-rank).
+int launch_wsum(int64_t len, int64_t stride, const double* x_all, const double* u_all, int n_local_nodes, double* wsum,
+                cudaStream_t s);
+// u_ij += x_ij - z_j and per-CTA partials of ||x_ij - z_j||^2.
+int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s);
+// node_sq[i] = sum over local blocks of node i (blocks[] order) of partials.
+int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq,
+                   cudaStream_t s);
+int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s);
+constexpr int kUThreads = 256;
+
+}  // namespace bic

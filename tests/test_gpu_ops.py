@@ -1,0 +1,222 @@
+"""GPU parity of each hot-path step (bicadmm_ops.h entry points, i.e. the same
+kernels the solver launches) against the FP64 oracle, element by element, on
+seeded inputs spanning several tiles and a ragged tail.
+
+Tolerances: FP64 storage -> 1e-12 relative (reduction-order rounding only);
+FP32 storage of A -> compared with the oracle on the same FP32-rounded matrix
+in FP64 (the kernels accumulate in FP64), so also ~1e-12."""
+import ctypes as ct
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bc():
+    from paper_2405_16267_b200 import build
+    build.build()
+    from paper_2405_16267_b200 import bicadmm
+    bicadmm.lib()
+    assert torch.cuda.is_available()
+    return bicadmm
+
+
+def _p(t):
+    return ct.c_void_p(t.data_ptr())
+
+
+def _s():
+    return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+SHAPES = [(1, 1), (7, 3), (300, 50), (1037, 513), (2050, 1026), (129, 4099)]
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("m,nj", SHAPES)
+def test_gemv(bc, orc, dt, m, nj):
+    rng = np.random.default_rng(m * 7 + nj)
+    lda = -(-nj // 4) * 4 + 4
+    Ah = rng.normal(size=(m, lda))
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    A = torch.tensor(Ah, dtype=tdt, device="cuda")
+    x = torch.tensor(rng.normal(size=nj), dtype=torch.float64, device="cuda")
+    y = torch.zeros(m, dtype=torch.float64, device="cuda")
+    bc.check(bc.lib().bicadmm_op_gemv(bc.F64 if dt == "f64" else bc.F32, m, nj, _p(A), lda, _p(x), _p(y), _s()))
+    torch.cuda.synchronize()
+    Aref = A.double().cpu().numpy()[:, :nj]
+    ref = orc.gemv(Aref, x.cpu().numpy())
+    assert _rel(y.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("m,nj", SHAPES)
+def test_gemv_t(bc, orc, dt, m, nj):
+    rng = np.random.default_rng(m * 3 + nj)
+    lda = -(-nj // 4) * 4
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    A = torch.tensor(rng.normal(size=(m, lda)), dtype=tdt, device="cuda")
+    p = torch.tensor(rng.normal(size=m), dtype=torch.float64, device="cuda")
+    d = torch.tensor(rng.normal(size=m), dtype=torch.float64, device="cuda")
+    z = torch.tensor(rng.normal(size=nj), dtype=torch.float64, device="cuda")
+    u = torch.tensor(rng.normal(size=nj), dtype=torch.float64, device="cuda")
+    r = torch.zeros(nj, dtype=torch.float64, device="cuda")
+    dtc = bc.F64 if dt == "f64" else bc.F32
+    wsb = bc.lib().bicadmm_op_gemv_t_ws(dtc, m, nj)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    bc.check(bc.lib().bicadmm_op_gemv_t(dtc, m, nj, _p(A), lda, _p(p), _p(d), _p(z), _p(u), 4.0, 2.5, _p(r),
+                                        _p(ws), wsb, _s()))
+    torch.cuda.synchronize()
+    Aref = A.double().cpu().numpy()[:, :nj]
+    q = p.cpu().numpy() + d.cpu().numpy()
+    ref = 4.0 * orc.gemv_t(Aref, q) + 2.5 * (z.cpu().numpy() - u.cpu().numpy())
+    assert _rel(r.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("loss", ["ls", "logistic", "hinge"])
+@pytest.mark.parametrize("M", [1, 3, 8])
+def test_prox(bc, orc, loss, M):
+    rng = np.random.default_rng(M)
+    m = 3001
+    b = rng.normal(size=m) if loss == "ls" else np.where(rng.random(m) < 0.5, -1.0, 1.0)
+    S = rng.normal(size=m) * 3
+    nu = rng.normal(size=m)
+    rho_l = 4.0
+    tb = torch.tensor(b, device="cuda")
+    tS = torch.tensor(S, device="cuda")
+    tnu = torch.tensor(nu, device="cuda")
+    td = torch.zeros(m, dtype=torch.float64, device="cuda")
+    tom = torch.zeros(m, dtype=torch.float64, device="cuda")
+    lid = bc.LOSSES[loss]
+    bc.check(bc.lib().bicadmm_op_prox(lid, bc.F64, 1, m, M, rho_l, _p(tb), _p(tS), _p(tnu), _p(td), _p(tom), _s()))
+    torch.cuda.synchronize()
+    abar = S / M
+    om = np.array([orc.prox_omega(lid, M, rho_l, b[r], [abar[r] + nu[r]])[0] for r in range(m)])
+    nu_new = nu + abar - om
+    delta = om - abar - nu_new
+    assert np.max(np.abs(tom.cpu().numpy() - om) / np.maximum(1, np.abs(om))) <= 1e-14
+    assert np.max(np.abs(tnu.cpu().numpy() - nu_new)) <= 1e-13
+    assert np.max(np.abs(td.cpu().numpy() - delta)) <= 1e-13
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("m,nj", [(40, 3), (300, 64), (1000, 130), (700, 257)])
+def test_block_factor(bc, orc, dt, m, nj):
+    rng = np.random.default_rng(nj)
+    lda = -(-nj // 4) * 4
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    Ah = rng.normal(size=(m, lda)) / np.sqrt(m)
+    A = torch.tensor(Ah, dtype=tdt, device="cuda")
+    rho_l, c = 4.0, 4.0025
+    ldh = lda
+    H = torch.zeros(nj, ldh, dtype=tdt, device="cuda")
+    dtc = bc.F64 if dt == "f64" else bc.F32
+    wsb = bc.lib().bicadmm_op_block_factor_ws(nj)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    bc.check(bc.lib().bicadmm_op_block_factor(dtc, m, nj, _p(A), lda, rho_l, c, _p(H), ldh, _p(ws), wsb, _s()))
+    torch.cuda.synchronize()
+    Aref = A.double().cpu().numpy()[:, :nj]
+    L = orc.block_factor(Aref, rho_l, c)
+    F = L @ L.T
+    Hn = H.double().cpu().numpy()[:, :nj]
+    tol = 1e-13 if dt == "f64" else 2e-7
+    assert np.max(np.abs(Hn @ F - np.eye(nj))) <= tol * 10
+    rhs = rng.normal(size=nj)
+    assert _rel(Hn @ rhs, orc.chol_solve(L, rhs)) <= tol
+    assert np.array_equal(Hn, Hn.T)
+
+
+@pytest.mark.parametrize("m,nj", [(33, 5), (517, 70), (2000, 129)])
+def test_gram(bc, m, nj):
+    rng = np.random.default_rng(m)
+    A = torch.tensor(rng.normal(size=(m, -(-nj // 4) * 4)), device="cuda")
+    G = torch.zeros(nj, nj, dtype=torch.float64, device="cuda")
+    bc.check(bc.lib().bicadmm_op_gram(bc.F64, m, nj, _p(A), A.stride(0), 2.0, 0.5, _p(G), nj, _s()))
+    torch.cuda.synchronize()
+    An = A.cpu().numpy()[:, :nj]
+    ref = 2.0 * An.T @ An + 0.5 * np.eye(nj)
+    assert np.max(np.abs(G.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+ZT_CASES = []
+_rng = np.random.default_rng(42)
+for _k in range(12):
+    _n = int(_rng.choice([2, 50, 1000, 4097, 30011]))
+    _w = _rng.normal(size=_n)
+    _sv = np.zeros(_n)
+    _idx = _rng.choice(_n, size=min(_n, 5), replace=False)
+    _sv[_idx] = _rng.uniform(-1, 1, size=_idx.size) if _k % 3 else np.sign(_w[_idx])
+    _v = float(_rng.normal() * (0.1 if _k % 4 else 10))
+    ZT_CASES.append((_w, _sv, _v, int(_rng.integers(1, 9)), float(_rng.choice([1.0, 4.0])), float(_rng.choice([0.5, 1.0]))))
+ZT_CASES.append((np.array([2.0, 1.0]), np.array([1.0, 0.0]), 0.0, 1, 1.0, 1.0))
+ZT_CASES.append((np.array([1.0, -2.0, 0.5]), np.array([1.0, -1.0, 0.0]), 1.0, 3, 2.0, 0.5))  # case 1
+ZT_CASES.append((np.zeros(7), np.zeros(7), -1.0, 2, 1.0, 0.5))                              # all zero
+
+
+@pytest.mark.parametrize("case", range(len(ZT_CASES)))
+def test_zt(bc, orc, case):
+    w, s, v, N, rho_c, alpha = ZT_CASES[case]
+    rho_b = alpha * rho_c
+    n = w.size
+    wsum = torch.tensor(w * N, device="cuda")       # the kernel divides by N
+    ts = torch.tensor(s, device="cuda")
+    wbar = torch.zeros(n, dtype=torch.float64, device="cuda")
+    z = torch.tensor(np.full(n, 0.25), device="cuda")
+    zp = torch.zeros(n, dtype=torch.float64, device="cuda")
+    out = (ct.c_double * 4)()
+    bc.check(bc.lib().bicadmm_op_zt(n, N, rho_c, rho_b, _p(wsum), _p(ts), v, _p(wbar), _p(z), _p(zp), out, _s()))
+    wb = (w * N) / N
+    zr, tr, taur = orc.zt_update(wb, s, v, N, rho_c, rho_b)
+    zg = z.cpu().numpy()
+    assert np.max(np.abs(zg - zr)) <= 1e-12 * max(1.0, np.max(np.abs(zr)))
+    assert abs(out[0] - tr) <= 1e-12 * max(1.0, abs(tr))
+    assert abs(out[1] - taur) <= 1e-12 * max(1.0, abs(taur))
+    assert np.all(zp.cpu().numpy() == 0.25)
+    assert out[2] == pytest.approx(np.sum((zg - 0.25) ** 2), rel=1e-12, abs=1e-300)
+
+
+S_CASES = []
+_rng = np.random.default_rng(7)
+for _k in range(10):
+    _n = int(_rng.choice([1, 3, 100, 5000, 40000]))
+    _z = _rng.normal(size=_n)
+    if _k % 3 == 0:
+        _z = np.round(_z * 2) / 2          # many ties
+    if _k % 4 == 1:
+        _z[_rng.random(_n) < 0.7] = 0.0    # many zeros
+    S_CASES.append((_z, float(_rng.normal() * 3), float(_rng.normal()), int(_rng.integers(0, _n + 2))))
+S_CASES.append((np.array([3.0, 1.0, -2.0]), 10.0, 0.0, 2))
+S_CASES.append((np.array([3.0, 1.0, -2.0]), 2.5, 0.0, 2))
+S_CASES.append((np.array([1.0, -1.0, 1.0, 0.5]), 10.0, 0.0, 2))  # ties -> lower index
+
+
+@pytest.mark.parametrize("case", range(len(S_CASES)))
+def test_s_update_and_support(bc, orc, case):
+    z, t, v, kappa = S_CASES[case]
+    n = z.size
+    tz = torch.tensor(z, device="cuda")
+    s = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+    out = (ct.c_double * 3)()
+    bc.check(bc.lib().bicadmm_op_s_update(n, kappa, _p(tz), t, v, _p(s), out, _s()))
+    sr, mcap = orc.s_update(z, t, v, kappa)
+    sg = s.cpu().numpy()
+    assert np.array_equal(sg != 0, sr != 0)             # identical selection T (integer decision)
+    assert np.max(np.abs(sg - sr)) <= 1e-14             # scale differs only by Mcap's summation order
+    assert out[0] == pytest.approx(mcap, rel=1e-13, abs=0)
+    g = float(z @ sr - t)
+    assert out[1] == pytest.approx(g, rel=1e-12, abs=1e-12 * max(1, abs(t)))
+    # support: top-kappa of |z| among nonzeros, ties to the lower index, ascending
+    sup = torch.zeros(max(kappa, 1), dtype=torch.int64, device="cuda")
+    cnt = (ct.c_int64 * 1)()
+    bc.check(bc.lib().bicadmm_op_support(n, kappa, _p(tz), _p(sup), cnt, _s()))
+    order = sorted(range(n), key=lambda l: (-abs(z[l]), l))
+    ref = sorted(l for l in order[:min(kappa, n)] if z[l] != 0.0)
+    assert cnt[0] == len(ref)
+    assert sup.cpu().numpy()[:cnt[0]].tolist() == ref

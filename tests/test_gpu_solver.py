@@ -1,0 +1,138 @@
+"""End-to-end GPU parity: the whole hot path through the C ABI (bicadmm_setup /
+bicadmm_iterate / bicadmm_finalize) against the oracle's run on the same seeded
+inputs, iterate by iterate.
+
+Bar (north star; DESIGN R22): FP64 -> every outer iterate z^k, t^k, v^k and the
+residuals within 1e-9 relative, identical support, objective within 1e-9.
+FP32 storage -> within 1e-4 against the oracle run on the FP64 data, identical
+support."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2405_16267_b200 import datagen as dg  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def bc():
+    from paper_2405_16267_b200 import build
+    build.build()
+    from paper_2405_16267_b200 import bicadmm
+    bicadmm.lib()
+    return bicadmm
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+def run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, seed=0, dtype=torch.float64, **kw):
+    P = dg.generate(N, m, n, kappa, loss, seed=seed)
+    cs = dg.block_partition(n, M)
+    oprm = dict(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0, **kw)
+    solver = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], loss,
+                        bc.Params(**oprm), cs)
+    zs, xs = [], []
+    for _ in range(K):
+        solver.iterate(1)
+        zs.append(solver.z)
+        xs.append(solver.get(bc.FIELD_X_LOCAL))
+    rep = solver.finalize()
+    lid = {"ls": orc.LS, "logistic": orc.LOGISTIC, "hinge": orc.HINGE}[loss]
+    Aref = [a.to(dtype).double().numpy() for a in P.A]
+    bref = [b.to(dtype).double().numpy() for b in P.b]
+    ref = orc.run(orc.Problem(Aref, bref, lid, 1, np.array(cs)), orc.Params(**oprm), trace_z=True, trace_x=True)
+    return solver, rep, np.array(zs), np.array(xs), ref, P
+
+
+CASES = [
+    # name, N, m_i, n, kappa, loss, M, K_outer, K_in
+    ("c1_ls", 2, 100, 50, 5, "ls", 1, 40, 10),
+    ("ls_blocks3", 2, 300, 250, 12, "ls", 3, 25, 5),
+    ("logistic_c2_replica", 4, 600, 300, 10, "logistic", 1, 20, 10),
+    ("hinge_blocks2", 3, 400, 201, 8, "hinge", 2, 20, 5),
+    ("logistic_blocks4_ragged", 2, 1037, 1030, 15, "logistic", 4, 8, 4),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fp64_iterates_match_oracle(bc, orc, case):
+    _, N, m, n, kappa, loss, M, K, K_in = case
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in)
+    tr_g = solver.trace()
+    tr_o = ref["trace"]
+    assert tr_g.shape == tr_o.shape
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, (k, _rel(zs[k], ref["z_trace"][k]))
+        # x_i (local blocks concatenated in node order = full x_i for single-rank placement)
+        assert _rel(xs[k], ref["x_trace"][k].ravel()) <= 1e-9, k
+        t_o, v_o = tr_o[k, 3], tr_o[k, 4]
+        assert abs(tr_g[k, 3] - t_o) <= 1e-9 * max(abs(t_o), 1e-300)
+        assert abs(tr_g[k, 4] - v_o) <= 1e-9 * max(abs(v_o), abs(t_o))
+        for c in (0, 1):   # p_r, d_r relative to their first-iteration scale (DESIGN R22)
+            assert abs(tr_g[k, c] - tr_o[k, c]) <= 1e-9 * max(abs(tr_o[k, c]), abs(tr_o[0, c]))
+        assert abs(tr_g[k, 2] - tr_o[k, 2]) <= 1e-9 * max(abs(tr_o[k, 2]), abs(t_o))
+    assert solver.support().tolist() == ref["support"].tolist()
+    assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
+
+
+def test_c1_solve_to_tolerance_recovers_brute_force_support(bc, orc):
+    # configs[0]: solve to eps = 1e-4 on the GPU; support equals exhaustive best subset
+    P = dg.generate(2, 100, 50, 5, "ls", seed=3)
+    cs = dg.block_partition(50, 1)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls",
+                        bc.Params(kappa=5, max_outer=2000, inner_fixed=10), cs)
+    rep = solver.solve()
+    pb = orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LS, 1, np.array(cs))
+    sup, _, _ = orc.best_subset(pb, 100.0, 5)
+    assert rep.converged == 1
+    assert solver.support().tolist() == sup.tolist()
+    ref = orc.run(pb, orc.Params(kappa=5, max_outer=2000, inner_fixed=10, refit=0))
+    assert rep.outer_iters == ref["iters"]
+    assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
+
+
+def test_fp32_mode_within_1e4(bc, orc):
+    # FP32 storage of A, b, H; FP64 iterates and accumulation (DESIGN R23)
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 4, 600, 300, 10, "logistic", 1, 15, 10, dtype=torch.float32)
+    for k in range(15):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-4, k
+    assert solver.support().tolist() == ref["support"].tolist()
+    assert abs(rep.objective - ref["objective"]) <= 1e-4 * abs(ref["objective"])
+
+
+def test_schedule_replay_matches_oracle(bc, orc):
+    # DESIGN R7: per-(outer, node) inner counts replayed identically on both sides
+    P = dg.generate(3, 200, 100, 6, "logistic", seed=5)
+    cs = dg.block_partition(100, 2)
+    K = 6
+    sched = np.array([[1, 4, 2], [3, 3, 1], [5, 1, 1], [2, 2, 2], [1, 1, 6], [4, 0, 3]], dtype=np.int32)
+    prm = dict(kappa=6, max_outer=K, inner_fixed=3, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(**prm), cs)
+    solver.set_schedule(sched)
+    solver.iterate(K)
+    ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs)),
+                  orc.Params(**prm), schedule=sched)
+    assert _rel(solver.z, ref["z"]) <= 1e-9
+    assert np.array_equal(solver.get(bc.FIELD_INNER_COUNTS, np.int32).reshape(K, 3), sched)
+
+
+def test_errors_and_domain(bc):
+    P = dg.generate(1, 40, 16, 2, "logistic", seed=1)
+    cs = dg.block_partition(16, 1)
+    bad = P.b[0].clone()
+    bad[3] = 0.5
+    with pytest.raises(bc.BicadmmError) as e:
+        bc.BiCADMM([P.A[0].cuda()], [bad.cuda()], "logistic", bc.Params(kappa=2), cs)
+    assert e.value.rc == bc.ERR_DOMAIN
+    with pytest.raises(bc.BicadmmError) as e:
+        bc.BiCADMM([P.A[0].cuda()], [P.b[0].cuda()], "logistic", bc.Params(kappa=17), cs)
+    assert e.value.rc == bc.ERR_INVALID
+    s = bc.BiCADMM([P.A[0].cuda()], [P.b[0].cuda()], "logistic", bc.Params(kappa=2, inner_fixed=2), cs)
+    s.iterate(2)
+    with pytest.raises(bc.BicadmmError):
+        s.iterate(-1)
+    assert s.launches() > 0
