@@ -8,6 +8,8 @@
 // enough independent loads in flight per SM (~40 KB) to cover DRAM latency.
 // Reductions are fixed-order (warp shuffle tree / per-chunk partials summed in
 // chunk order), so results are bitwise reproducible.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -133,7 +135,7 @@ __device__ __forceinline__ void gemv_rows_f32(const GemvDesc& D, int64_t r0, int
     }
 }
 
-template <typename T>
+template <typename T, int R>
 __global__ void __launch_bounds__(kGemvThreads) k_gemv(const __grid_constant__ GemvBatch B) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (kGemvThreads / 32);
@@ -142,13 +144,34 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(const __grid_constant__ G
         int di = 0;
         while (di + 1 < B.nd && task >= B.d[di + 1].task_begin) ++di;
         const GemvDesc& D = B.d[di];
-        const int64_t r0 = (task - D.task_begin) * kGemvR;
-        if constexpr (sizeof(T) == 8) gemv_rows_f64<kGemvR>(D, r0, lane);
-        else gemv_rows_f32<kGemvR>(D, r0, lane);
+        const int64_t r0 = (task - D.task_begin) * R;
+        if constexpr (sizeof(T) == 8) gemv_rows_f64<R>(D, r0, lane);
+        else gemv_rows_f32<R>(D, r0, lane);
+    }
+}
+
+// rows per warp-task: BICADMM_GEMV_R in {1, 2, 4, 8} (tuning), default kGemvR
+static int gemv_rows_per_task() {
+    static int r = [] {
+        const char* e = getenv("BICADMM_GEMV_R");
+        int v = e ? atoi(e) : kGemvR;
+        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : kGemvR;
+    }();
+    return r;
+}
+
+template <typename T>
+static void gemv_dispatch(int R, unsigned blocks, cudaStream_t s, const GemvBatch& B) {
+    switch (R) {
+    case 1: k_gemv<T, 1><<<blocks, kGemvThreads, 0, s>>>(B); break;
+    case 2: k_gemv<T, 2><<<blocks, kGemvThreads, 0, s>>>(B); break;
+    case 8: k_gemv<T, 8><<<blocks, kGemvThreads, 0, s>>>(B); break;
+    default: k_gemv<T, 4><<<blocks, kGemvThreads, 0, s>>>(B); break;
     }
 }
 
 int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s) {
+    const int R = gemv_rows_per_task();
     for (int base = 0; base < nd; base += kMaxDesc) {
         GemvBatch B;
         B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;
@@ -156,14 +179,18 @@ int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s) {
         for (int k = 0; k < B.nd; ++k) {
             B.d[k] = d[base + k];
             B.d[k].task_begin = t;
-            t += (B.d[k].rows + kGemvR - 1) / kGemvR;
+            t += (B.d[k].rows + R - 1) / R;
         }
         B.total_tasks = t;
         if (t == 0) continue;
         int64_t blocks = (t + (kGemvThreads / 32) - 1) / (kGemvThreads / 32);
-        if (blocks > grid_cap) blocks = grid_cap;
-        if (dtype == BICADMM_F64) k_gemv<double><<<(unsigned)blocks, kGemvThreads, 0, s>>>(B);
-        else k_gemv<float><<<(unsigned)blocks, kGemvThreads, 0, s>>>(B);
+        // default: one warp-task per warp (the block scheduler balances the tail);
+        // BICADMM_GEMV_PERSISTENT=1 caps the grid at the resident CTA count instead
+        static const bool persistent = getenv("BICADMM_GEMV_PERSISTENT") && atoi(getenv("BICADMM_GEMV_PERSISTENT"));
+        if (persistent && blocks > grid_cap) blocks = grid_cap;
+        if (blocks > 0x7fffffff) blocks = 0x7fffffff;
+        if (dtype == BICADMM_F64) gemv_dispatch<double>(R, (unsigned)blocks, s, B);
+        else gemv_dispatch<float>(R, (unsigned)blocks, s, B);
         BIC_LAUNCHED();
     }
     return BICADMM_OK;
@@ -171,8 +198,8 @@ int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s) {
 
 int gemv_grid_cap(int dtype, int sm_count) {
     int occ = 0;
-    if (dtype == BICADMM_F64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv<double>, kGemvThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv<float>, kGemvThreads, 0);
+    if (dtype == BICADMM_F64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv<double, kGemvR>, kGemvThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv<float, kGemvR>, kGemvThreads, 0);
     if (occ < 1) occ = 1;
     return occ * sm_count;
 }
