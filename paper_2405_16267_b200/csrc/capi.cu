@@ -127,6 +127,8 @@ struct bicadmm_handle {
     double *x_all = nullptr, *u_all = nullptr, *z = nullptr, *z_prev = nullptr, *s = nullptr, *wbar = nullptr,
            *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
            *fws = nullptr, *node_obj = nullptr;
+    double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
+    int refit_iters = 0;
     OuterScalars* sc = nullptr;
     int64_t* support = nullptr;
     int64_t* support_count = nullptr;
@@ -207,7 +209,7 @@ static int validate(const bicadmm_problem* P, const bicadmm_params* R, std::stri
     if (P->loss < 0 || P->loss > 3) { *why = "unknown loss"; return BICADMM_ERR_INVALID; }
     if (P->dtype != BICADMM_F64 && P->dtype != BICADMM_F32) { *why = "unknown dtype"; return BICADMM_ERR_INVALID; }
     if ((P->loss == BICADMM_SOFTMAX) != (P->C > 1)) { *why = "C > 1 iff softmax"; return BICADMM_ERR_DIM; }
-    if (P->C > 1) { *why = "softmax (C > 1) is not supported by this build's GPU path yet"; return BICADMM_ERR_INVALID; }
+    if (P->C > 16) { *why = "C <= 16 classes"; return BICADMM_ERR_INVALID; }
     if (P->col_start[0] != 0 || P->col_start[P->M] != P->n) { *why = "col_start must span [0, n]"; return BICADMM_ERR_DIM; }
     for (int j = 0; j < P->M; ++j) {
         if (P->col_start[j + 1] <= P->col_start[j]) { *why = "col_start not increasing"; return BICADMM_ERR_DIM; }
@@ -313,7 +315,7 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         h->gt[k].cols = h->blk[k].nj;
     }
     std::vector<int64_t> need(h->blk.size());
-    plan_gemv_t(P->dtype, h->gt.data(), (int)h->gt.size(), h->sm_count, need.data());
+    plan_gemv_t(P->dtype, h->gt.data(), (int)h->gt.size(), h->sm_count, need.data(), C);
     for (size_t k = 0; k < h->blk.size(); ++k) {
         LBlock& L = h->blk[k];
         LNode& nd = h->nod[L.li];
@@ -326,6 +328,12 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     }
     // setup scratch: FP64 Gram / factor workspace
     const int64_t ldg = rup(njmax, 8);
+    h->mask = b.arr<double>(len);
+    h->cg_r = b.arr<double>(len);
+    h->cg_p = b.arr<double>(len);
+    h->cg_Ap = b.arr<double>(len);
+    h->cg_rhs = b.arr<double>(len);
+    h->cg_sc = b.arr<double>(8);
     h->gram = b.arr<double>(ldg * njmax);
     h->fws = b.arr<double>((int64_t)factor_ws_doubles(njmax));
     return b.off + 256;
@@ -339,7 +347,7 @@ static void build_descs(bicadmm_handle* h) {
         GemvTDesc& g = h->gt[k];
         g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
         g.p = L.p; g.delta = h->nod[L.li].delta;
-        g.z = h->z + L.c0; g.u = L.u; g.r = L.r; g.partial = L.partial;
+        g.z = h->z + L.c0 * h->C; g.u = L.u; g.r = L.r; g.partial = L.partial;
     }
     h->bv.clear();
     for (auto& L : h->blk) {
@@ -583,12 +591,12 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes) 
     };
     mark(0);
     cudaEvent_t mid = h->prof ? next_event(h) : nullptr;
-    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid));
+    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid, h->C));
     const int64_t l_partial = (int64_t)(gt.size() + kMaxDesc - 1) / kMaxDesc;
     mark(2);
-    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st));
+    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st, h->C));
     mark(3);
-    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st));
+    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, h->C));
     mark(4);
     if (h->split_blocks) {
         H_RC(h, launch_psum(h->C, px.data(), (int)px.size(), nullptr, h->st));
@@ -712,19 +720,83 @@ __global__ void k_sqnorm(int64_t len, const double* __restrict__ x, double* out)
 
 // Support = top-kappa of |z| with z != 0 (ties to the lower index), x_final = z on
 // the support (DESIGN R19), objective (1) at x_final (DESIGN R20).
+// out = mask * (2 sum_i A_i^T (w_i) + lambda v), where w_i = sum_j A_ij v_j (use_v) or
+// w_i = b_i (rhs mode, lambda term dropped).  Same GEMV / GEMV-T kernels as the sweep.
+static int refit_apply(bicadmm_handle* h, const double* v, double* out, bool rhs_mode) {
+    if (!rhs_mode) {
+        std::vector<GemvDesc> ax;
+        for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, v + L.c0, L.pobj, 0});
+        H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, 1));
+        for (auto& nd : h->nod) {
+            ProxNode p{};
+            p.p = nd.pobj_base; p.np = nd.np; p.pstride = nd.m; p.m = nd.m; p.S = nd.S;
+            H_RC(h, launch_psum(1, &p, 1, nullptr, h->st));
+            if (h->split_blocks) H_RC(h, allreduce(h, nd.S, nd.m, true));
+        }
+    } else {
+        for (auto& nd : h->nod) H_RC(h, launch_to_f64(h->dtype, nd.m, nd.b, nd.S, h->st));
+    }
+    std::vector<GemvTDesc> gt;
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        GemvTDesc g = h->gt[k];
+        g.p = h->nod[h->blk[k].li].S; g.delta = nullptr; g.z = nullptr; g.u = nullptr;
+        gt.push_back(g);
+    }
+    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), 2.0, 0.0, h->st, nullptr, 1));
+    H_CUDA(h, cudaMemsetAsync(out, 0, sizeof(double) * h->len, h->st));
+    for (auto& L : h->blk) H_RC(h, launch_axpy_into(L.nj, L.r, out + L.c0, h->st));
+    H_RC(h, allreduce(h, out, h->len, false));
+    H_RC(h, launch_ridge_mask(h->len, h->mask, v, rhs_mode ? 0.0 : h->prm.lambda, out, h->st));
+    return BICADMM_OK;
+}
+
+// LS ridge refit on the support (DESIGN R19): CG on the SPD system restricted to T,
+// warm-started at z|_T, to a relative residual of 1e-14.
+static int do_refit(bicadmm_handle* h) {
+    const int64_t len = h->len;
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(h->prm.kappa, len));
+    H_CUDA(h, cudaMemsetAsync(h->mask, 0, sizeof(double) * len, h->st));
+    H_RC(h, launch_support_mask(cap, h->support, h->support_count, h->mask, h->st));
+    H_RC(h, refit_apply(h, nullptr, h->cg_rhs, true));                    // rhs = 2 A_T^T b
+    H_RC(h, refit_apply(h, h->x_final, h->cg_Ap, false));                 // A x0
+    H_CUDA(h, cudaMemcpyAsync(h->cg_r, h->cg_rhs, sizeof(double) * len, cudaMemcpyDeviceToDevice, h->st));
+    H_RC(h, launch_axpy_scaled(len, -1.0, h->cg_Ap, h->cg_r, h->st));    // r = rhs - A x0
+    H_CUDA(h, cudaMemcpyAsync(h->cg_p, h->cg_r, sizeof(double) * len, cudaMemcpyDeviceToDevice, h->st));
+    H_RC(h, launch_dot(len, h->cg_r, h->cg_r, h->cg_sc + 0, h->st));
+    H_RC(h, launch_dot(len, h->cg_rhs, h->cg_rhs, h->cg_sc + 3, h->st));
+    double hs[4] = {0, 0, 0, 0};
+    H_CUDA(h, cudaMemcpyAsync(hs, h->cg_sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    const double tol2 = 1e-28 * hs[3];
+    h->refit_iters = 0;
+    if (hs[0] <= tol2) return BICADMM_OK;
+    for (int it = 0; it < 500; ++it) {
+        H_RC(h, refit_apply(h, h->cg_p, h->cg_Ap, false));
+        H_RC(h, launch_dot(len, h->cg_p, h->cg_Ap, h->cg_sc + 1, h->st));
+        H_RC(h, launch_cg_xr(len, h->cg_sc, h->cg_p, h->cg_Ap, h->x_final, h->cg_r, h->st));
+        H_RC(h, launch_dot(len, h->cg_r, h->cg_r, h->cg_sc + 2, h->st));
+        H_RC(h, launch_cg_p(len, h->cg_sc, h->cg_r, h->cg_p, h->st));
+        H_CUDA(h, cudaMemcpyAsync(h->cg_sc, h->cg_sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+        H_CUDA(h, cudaMemcpyAsync(hs + 2, h->cg_sc + 2, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        H_CUDA(h, cudaStreamSynchronize(h->st));
+        h->refit_iters = it + 1;
+        if (!(hs[2] > tol2)) break;
+    }
+    return BICADMM_OK;
+}
+
 static int do_finalize(bicadmm_handle* h) {
     const int64_t len = h->len;
-    if (h->prm.refit && h->loss == BICADMM_LS)
-        return fail(h, BICADMM_ERR_INVALID, "LS refit on the support is not implemented in this build's GPU path; pass refit = 0");
     H_RC(h, launch_support(len, h->prm.kappa, h->z, h->support, h->support_count, h->st));
     H_CUDA(h, cudaMemsetAsync(h->x_final, 0, sizeof(double) * len, h->st));
     const int64_t kk = std::max<int64_t>(1, std::min<int64_t>(h->prm.kappa, len));
     k_scatter_support<<<(unsigned)((kk + 255) / 256), 256, 0, h->st>>>(h->z, h->support, h->support_count, h->x_final);
     BIC_LAUNCHED();
+    if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
     for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0});
-    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st));
+    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, h->C));
     std::vector<ProxNode> px;
     for (auto& nd : h->nod) {
         ProxNode p{};

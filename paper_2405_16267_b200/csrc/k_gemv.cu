@@ -26,7 +26,7 @@ struct GemvBatch {
     int64_t total_tasks;
 };
 
-constexpr int kGemvR = 4;          // rows per warp-task (x reuse across rows)
+constexpr int kGemvR = 1;          // rows per warp-task (measured best: R=1, 7.0 TB/s at C2, profiles/r01_microbench.jsonl)
 constexpr int kGemvThreads = 256;
 
 template <int R>
@@ -170,7 +170,8 @@ static void gemv_dispatch(int R, unsigned blocks, cudaStream_t s, const GemvBatc
     }
 }
 
-int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s) {
+int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s, int C) {
+    if (C > 1) return launch_gemv_c(dtype, C, d, nd, s);
     const int R = gemv_rows_per_task();
     for (int base = 0; base < nd; base += kMaxDesc) {
         GemvBatch B;
@@ -323,22 +324,23 @@ struct GemvTRedBatch {
 };
 
 __global__ void __launch_bounds__(256) k_gemv_t_reduce(const __grid_constant__ GemvTRedBatch B, double rho_l,
-                                                       double rho_c) {
+                                                       double rho_c, int C) {
     const int64_t cta = blockIdx.x;
     int di = 0;
     while (di + 1 < B.nd && cta >= B.cta_begin[di + 1]) ++di;
     const GemvTDesc& D = B.d[di];
     const int64_t c = (cta - B.cta_begin[di]) * 256 + threadIdx.x;
-    if (c >= D.cols) return;
+    const int64_t ncomp = D.cols * C;
+    if (c >= ncomp) return;
     double s = 0.0;
-    for (int k = 0; k < D.nchunks; ++k) s += D.partial[(int64_t)k * D.cols + c];
+    for (int k = 0; k < D.nchunks; ++k) s += D.partial[(int64_t)k * ncomp + c];
     double r = rho_l * s;
     if (D.z || D.u) r += rho_c * ((D.z ? D.z[c] : 0.0) - (D.u ? D.u[c] : 0.0));
     D.r[c] = r;
 }
 
-void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need) {
-    const int W = gemv_t_strip_width(dtype);
+void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need, int C) {
+    const int W = C > 1 ? gemv_t_c_strip_width(dtype) : gemv_t_strip_width(dtype);
     int64_t total_strips = 0;
     for (int k = 0; k < nd; ++k) {
         d[k].nstrips = (int32_t)((d[k].cols + W - 1) / W);
@@ -355,13 +357,18 @@ void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need) {
         d[k].chunk_rows = cr;
         d[k].nchunks = (int32_t)((d[k].rows + cr - 1) / cr);
         if (d[k].nchunks < 1) d[k].nchunks = 1;
-        need[k] = (int64_t)d[k].nchunks * d[k].cols;
+        need[k] = (int64_t)d[k].nchunks * d[k].cols * C;
     }
 }
 
-int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s, cudaEvent_t mid) {
+int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s, cudaEvent_t mid,
+                  int C) {
     // all partial passes first (the HBM pass over A), then the chunk reductions
-    for (int base = 0; base < nd; base += kMaxDesc) {
+    if (C > 1) {
+        int rc = launch_gemv_t_c_partial(dtype, C, d, nd, s);
+        if (rc) return rc;
+    }
+    for (int base = 0; base < nd && C == 1; base += kMaxDesc) {
         GemvTBatch B;
         B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;
         int64_t t = 0;
@@ -385,10 +392,10 @@ int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, c
         for (int k = 0; k < R.nd; ++k) {
             R.d[k] = d[base + k];
             R.cta_begin[k] = tr;
-            tr += (R.d[k].cols + 255) / 256;
+            tr += (R.d[k].cols * C + 255) / 256;
         }
         if (tr > 0) {
-            k_gemv_t_reduce<<<(unsigned)tr, 256, 0, s>>>(R, rho_l, rho_c);
+            k_gemv_t_reduce<<<(unsigned)tr, 256, 0, s>>>(R, rho_l, rho_c, C);
             BIC_LAUNCHED();
         }
     }

@@ -15,7 +15,8 @@ struct GemvDesc {
     double* y;
     int64_t task_begin;  // filled by the launcher
 };
-int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s);
+int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s, int C = 1);
+int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
 int gemv_grid_cap(int dtype, int sm_count);  // persistent grid size (resident CTAs)
 
 // r[l] = rho_l * sum_r A[r, l] (p[r] + delta[r]) + rho_c (z[l] - u[l])   (Eq. (24))
@@ -34,9 +35,11 @@ struct GemvTDesc {
 };
 // Choose chunk_rows / nchunks for a batch so the grid fills the GPU; returns
 // scratch doubles needed by descriptor k in need[k].
-void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need);
+void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need, int C = 1);
 int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s,
-                  cudaEvent_t mid = nullptr);
+                  cudaEvent_t mid = nullptr, int C = 1);
+int launch_gemv_t_c_partial(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s);
+int gemv_t_c_strip_width(int dtype);
 int gemv_t_strip_width(int dtype);
 
 // ---------------------------------------------------------------- prox (Eqs. (22), (23))
@@ -98,5 +101,15 @@ int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, dou
                    cudaStream_t s);
 int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s);
 constexpr int kUThreads = 256;
+
+// ---------------------------------------------------------------- finalize vectors (k_vec.cu)
+int launch_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
+int launch_ridge_mask(int64_t n, const double* mask, const double* v, double lambda, double* y, cudaStream_t s);
+int launch_cg_xr(int64_t n, const double* sc, const double* p, const double* Ap, double* x, double* r, cudaStream_t s);
+int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStream_t s);
+int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s);
+int launch_support_mask(int64_t cap, const int64_t* sup, const int64_t* cnt, double* mask, cudaStream_t s);
+int launch_axpy_into(int64_t n, const double* x, double* y, cudaStream_t s);          // y += x
+int launch_axpy_scaled(int64_t n, double a, const double* x, double* y, cudaStream_t s);  // y += a x
 
 }  // namespace bic

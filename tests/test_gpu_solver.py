@@ -29,28 +29,30 @@ def _rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
 
 
-def run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, seed=0, dtype=torch.float64, **kw):
-    P = dg.generate(N, m, n, kappa, loss, seed=seed)
+def run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, seed=0, dtype=torch.float64, C=1, **kw):
+    P = dg.generate(N, m, n, kappa, loss, seed=seed, C=C)
     cs = dg.block_partition(n, M)
     oprm = dict(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0, **kw)
     solver = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], loss,
-                        bc.Params(**oprm), cs)
+                        bc.Params(**oprm), cs, C=P.C)
     zs, xs = [], []
     for _ in range(K):
         solver.iterate(1)
         zs.append(solver.z)
         xs.append(solver.get(bc.FIELD_X_LOCAL))
     rep = solver.finalize()
-    lid = {"ls": orc.LS, "logistic": orc.LOGISTIC, "hinge": orc.HINGE}[loss]
+    lid = {"ls": orc.LS, "logistic": orc.LOGISTIC, "hinge": orc.HINGE, "softmax": orc.SOFTMAX}[loss]
     Aref = [a.to(dtype).double().numpy() for a in P.A]
     bref = [b.to(dtype).double().numpy() for b in P.b]
-    ref = orc.run(orc.Problem(Aref, bref, lid, 1, np.array(cs)), orc.Params(**oprm), trace_z=True, trace_x=True)
+    ref = orc.run(orc.Problem(Aref, bref, lid, P.C, np.array(cs)), orc.Params(**oprm), trace_z=True, trace_x=True)
     return solver, rep, np.array(zs), np.array(xs), ref, P
 
 
 CASES = [
-    # name, N, m_i, n, kappa, loss, M, K_outer, K_in
+    # name, N, m_i, n, kappa, loss, M, K_outer, K_in[, C]
     ("c1_ls", 2, 100, 50, 5, "ls", 1, 40, 10),
+    ("softmax_c4_replica_M8", 1, 1500, 200, 20, "softmax", 8, 8, 4, 10),
+    ("softmax_c3_blocks2", 2, 300, 61, 6, "softmax", 2, 10, 5, 3),
     ("ls_blocks3", 2, 300, 250, 12, "ls", 3, 25, 5),
     ("logistic_c2_replica", 4, 600, 300, 10, "logistic", 1, 20, 10),
     ("hinge_blocks2", 3, 400, 201, 8, "hinge", 2, 20, 5),
@@ -60,8 +62,9 @@ CASES = [
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_fp64_iterates_match_oracle(bc, orc, case):
-    _, N, m, n, kappa, loss, M, K, K_in = case
-    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in)
+    _, N, m, n, kappa, loss, M, K, K_in = case[:9]
+    C = case[9] if len(case) > 9 else 1
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C)
     tr_g = solver.trace()
     tr_o = ref["trace"]
     assert tr_g.shape == tr_o.shape
@@ -136,3 +139,20 @@ def test_errors_and_domain(bc):
     with pytest.raises(bc.BicadmmError):
         s.iterate(-1)
     assert s.launches() > 0
+
+
+@pytest.mark.parametrize("M", [1, 3])
+def test_ls_refit_matches_oracle(bc, orc, M):
+    # a13 / DESIGN R19: ridge refit on the support; GPU CG vs oracle Cholesky
+    P = dg.generate(3, 120, 60, 6, "ls", seed=11)
+    cs = dg.block_partition(60, M)
+    prm = dict(kappa=6, max_outer=30, inner_fixed=8, refit=1, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls", bc.Params(**prm), cs)
+    solver.iterate(30)
+    rep = solver.finalize()
+    ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LS, 1, np.array(cs)),
+                  orc.Params(**prm))
+    assert solver.support().tolist() == ref["support"].tolist()
+    xf = solver.get(bc.FIELD_X_FINAL)
+    assert _rel(xf, ref["x_final"]) <= 1e-9
+    assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
