@@ -127,6 +127,7 @@ struct bicadmm_handle {
     double *x_all = nullptr, *u_all = nullptr, *z = nullptr, *z_prev = nullptr, *s = nullptr, *wbar = nullptr,
            *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
            *fws = nullptr, *node_obj = nullptr;
+    double *x_old = nullptr, *dpart = nullptr, *node_dx = nullptr, *node_res = nullptr;
     double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
     int refit_iters = 0;
     OuterScalars* sc = nullptr;
@@ -297,6 +298,10 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     int64_t uparts = 0;
     for (auto& L : h->blk) uparts += (L.nj * C + kUThreads * 4 - 1) / (kUThreads * 4);
     h->upart = b.arr<double>(uparts);
+    h->dpart = b.arr<double>(uparts);
+    h->x_old = b.arr<double>(lenp * nl);
+    h->node_dx = b.arr<double>(P->N);
+    h->node_res = b.arr<double>(P->N);
     // per node
     for (auto& nd : h->nod) {
         nd.nu = b.arr<double>(nd.m * C);
@@ -558,7 +563,7 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
 }
 
 // ======================================================================= iterate
-static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes) {
+static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, bool tol = false) {
     // descriptors for the active nodes' blocks
     std::vector<GemvTDesc> gt;
     std::vector<GemvDesc> hx, ax;
@@ -578,7 +583,8 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes) 
         const LNode& nd = h->nod[li];
         ProxNode p{};
         p.b = nd.b; p.p = nd.p_base; p.S = h->split_blocks ? nd.S : nullptr; p.nu = nd.nu; p.delta = nd.delta;
-        p.omega = nullptr; p.sq_partial = nullptr; p.m = nd.m; p.pstride = nd.m * h->C; p.np = nd.np;
+        p.omega = nullptr; p.sq_partial = tol ? nd.sq_partial : nullptr; p.m = nd.m; p.pstride = nd.m * h->C;
+        p.np = nd.np;
         px.push_back(p);
     }
     cudaEvent_t ev[7] = {};
@@ -594,6 +600,9 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes) 
     H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid, h->C));
     const int64_t l_partial = (int64_t)(gt.size() + kMaxDesc - 1) / kMaxDesc;
     mark(2);
+    if (tol)   // keep x^k for the ||x^{k+1} - x^k|| criterion
+        H_CUDA(h, cudaMemcpyAsync(h->x_old, h->x_all, sizeof(double) * h->lenp * h->nod.size(),
+                                  cudaMemcpyDeviceToDevice, h->st));
     H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st, h->C));
     mark(3);
     H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, h->C));
@@ -644,6 +653,41 @@ static int outer_step(bicadmm_handle* h) {
     return BICADMM_OK;
 }
 
+// Per-node inner criteria after a tol-mode sweep: res[i] = ||abar_i - obar_i||^2,
+// dx[i] = ||x_i^new - x_i^old||^2 (both FP64, fixed-order sums; dx all-reduced over
+// the node group when a node's blocks span ranks).
+static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std::vector<double>& res,
+                          std::vector<double>& dx) {
+    std::vector<BlockVec> bv;
+    for (auto& L : h->blk) {
+        bool on = false;
+        for (int li : active) on |= li == L.li;
+        if (!on) continue;
+        BlockVec v{};
+        v.x = L.x; v.u = h->x_old + (L.x - h->x_all); v.c0 = 0; v.len = L.nj * h->C; v.node = L.node;
+        bv.push_back(v);
+    }
+    H_CUDA(h, cudaMemsetAsync(h->node_dx, 0, sizeof(double) * h->N, h->st));
+    H_RC(h, launch_u_update(bv.data(), (int)bv.size(), nullptr, h->dpart, h->st, 1));
+    H_RC(h, launch_node_sq(bv.data(), (int)bv.size(), h->dpart, h->N, h->node_dx, h->st));
+    if (h->split_blocks) H_RC(h, allreduce(h, h->node_dx, h->N, true));
+    std::vector<const double*> ptr;
+    std::vector<int64_t> cnt;
+    std::vector<int32_t> node;
+    for (int li : active) {
+        ptr.push_back(h->nod[li].sq_partial);
+        cnt.push_back(h->nod[li].nprox_ctas);
+        node.push_back(h->nod[li].node);
+    }
+    H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));
+    res.assign(h->N, 0.0);
+    dx.assign(h->N, 0.0);
+    H_CUDA(h, cudaMemcpyAsync(res.data(), h->node_res, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaMemcpyAsync(dx.data(), h->node_dx, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    return BICADMM_OK;
+}
+
 static int sweeps_for(bicadmm_handle* h, int k, int li) {
     if (!h->schedule.empty()) {
         const int row = k - h->sched_start;
@@ -656,22 +700,46 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
     if (!h) return BICADMM_ERR_INVALID;
     if (h->dead) return BICADMM_ERR_STATE;
     if (n_outer < 0) return fail(h, BICADMM_ERR_INVALID, "n_outer < 0");
-    if (h->prm.inner_fixed == 0 && h->schedule.empty())
-        return fail(h, BICADMM_ERR_INVALID, "tolerance-mode inner loop is not implemented in this build; use inner_fixed > 0 or a schedule");
     int sweeps_call = 0;
     for (int it = 0; it < n_outer; ++it) {
         const int k = h->outer_done;
+        const int srow = k - h->sched_start;
+        const bool replay = !h->schedule.empty() && srow >= 0 && srow < h->sched_rows;
+        const bool tol = !replay && h->prm.inner_fixed == 0;
         std::vector<int> want(h->nod.size());
         int maxs = 0;
-        for (size_t li = 0; li < h->nod.size(); ++li) {
-            want[li] = sweeps_for(h, k, (int)li);
-            maxs = std::max(maxs, want[li]);
-        }
-        for (int sw = 0; sw < maxs; ++sw) {
+        if (!tol) {
+            for (size_t li = 0; li < h->nod.size(); ++li) {
+                want[li] = sweeps_for(h, k, (int)li);
+                maxs = std::max(maxs, want[li]);
+            }
+            for (int sw = 0; sw < maxs; ++sw) {
+                std::vector<int> active;
+                for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);
+                int rc = inner_sweep(h, active);
+                if (rc) return rc;
+            }
+        } else {
+            // tolerance mode: sweep node i until ||abar - obar|| <= eps sqrt(m_i C) and
+            // ||x_i^new - x_i^old|| <= eps, at most max_inner sweeps
             std::vector<int> active;
-            for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);
-            int rc = inner_sweep(h, active);
-            if (rc) return rc;
+            for (size_t li = 0; li < h->nod.size(); ++li) active.push_back((int)li);
+            std::vector<double> res, dx;
+            for (int sw = 0; sw < h->prm.max_inner && !active.empty(); ++sw) {
+                int rc = inner_sweep(h, active, true);
+                if (!rc) rc = inner_criteria(h, active, res, dx);
+                if (rc) return rc;
+                std::vector<int> still;
+                for (int li : active) {
+                    want[li] = sw + 1;
+                    const int i = h->nod[li].node;
+                    const bool done = std::sqrt(res[i]) <= h->prm.eps_inner * std::sqrt((double)(h->nod[li].m * h->C)) &&
+                                      std::sqrt(dx[i]) <= h->prm.eps_inner;
+                    if (!done) still.push_back(li);
+                }
+                active.swap(still);
+                maxs = sw + 1;
+            }
         }
         int rc = outer_step(h);
         if (rc) return rc;
@@ -746,7 +814,7 @@ static int refit_apply(bicadmm_handle* h, const double* v, double* out, bool rhs
     H_CUDA(h, cudaMemsetAsync(out, 0, sizeof(double) * h->len, h->st));
     for (auto& L : h->blk) H_RC(h, launch_axpy_into(L.nj, L.r, out + L.c0, h->st));
     H_RC(h, allreduce(h, out, h->len, false));
-    H_RC(h, launch_ridge_mask(h->len, h->mask, v, rhs_mode ? 0.0 : h->prm.lambda, out, h->st));
+    H_RC(h, launch_ridge_mask(h->len, h->mask, rhs_mode ? out : v, rhs_mode ? 0.0 : h->prm.lambda, out, h->st));
     return BICADMM_OK;
 }
 

@@ -313,8 +313,10 @@ struct UBatch {
 };
 constexpr int kUPer = 4;  // elements per thread
 
+// mode 0: u_ij += x_ij - z_j, partials of ||x_ij - z_j||^2   (Eq. (9) + Eq. (15) p_r)
+// mode 1: partials of ||x_ij - u_ij||^2 with u := x_old            (inner tol criterion)
 __global__ void __launch_bounds__(kUThreads) k_u_update(const __grid_constant__ UBatch B, const double* __restrict__ z,
-                                                        double* __restrict__ partial, int64_t partial_base) {
+                                                        double* __restrict__ partial, int64_t partial_base, int mode) {
     __shared__ double scratch[32];
     const int64_t cta = blockIdx.x;
     int bi = 0;
@@ -326,17 +328,22 @@ __global__ void __launch_bounds__(kUThreads) k_u_update(const __grid_constant__ 
     for (int k = 0; k < kUPer; ++k) {
         const int64_t e = e0 + threadIdx.x + k * kUThreads;
         if (e < V.len) {
-            const double x = V.x[e], zl = z[V.c0 + e];
-            const double d = x - zl;
-            V.u[e] += d;
-            sq += d * d;
+            const double x = V.x[e];
+            if (mode == 0) {
+                const double d = x - z[V.c0 + e];
+                V.u[e] += d;
+                sq += d * d;
+            } else {
+                const double d = x - V.u[e];
+                sq += d * d;
+            }
         }
     }
     sq = block_sum(sq, scratch);
     if (threadIdx.x == 0) partial[partial_base + cta] = sq;
 }
 
-int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s) {
+int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s, int mode) {
     int64_t base = 0;
     for (int b0 = 0; b0 < nb; b0 += kMaxDesc) {
         UBatch B;
@@ -349,10 +356,37 @@ int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cuda
             t += (B.b[k].len + kUThreads * kUPer - 1) / (kUThreads * kUPer);
         }
         if (t > 0) {
-            k_u_update<<<(unsigned)t, kUThreads, 0, s>>>(B, z, partial, base);
+            k_u_update<<<(unsigned)t, kUThreads, 0, s>>>(B, z, partial, base, mode);
             BIC_LAUNCHED();
         }
         base += t;
+    }
+    return BICADMM_OK;
+}
+
+// out[node[k]] = sum of parts[k][0..count[k]) (fixed order) for each listed node
+struct SegArgs {
+    const double* ptr[kMaxDesc];
+    int64_t count[kMaxDesc];
+    int32_t node[kMaxDesc];
+    int n;
+};
+__global__ void k_seg_sums(const __grid_constant__ SegArgs A, double* __restrict__ out) {
+    for (int k = threadIdx.x; k < A.n; k += blockDim.x) {
+        double s = 0.0;
+        for (int64_t e = 0; e < A.count[k]; ++e) s += A.ptr[k][e];
+        out[A.node[k]] = s;
+    }
+}
+
+int launch_seg_sums(const double* const* ptr, const int64_t* count, const int32_t* node, int n, double* out,
+                    cudaStream_t s) {
+    for (int b0 = 0; b0 < n; b0 += kMaxDesc) {
+        SegArgs A;
+        A.n = n - b0 < kMaxDesc ? n - b0 : kMaxDesc;
+        for (int k = 0; k < A.n; ++k) { A.ptr[k] = ptr[b0 + k]; A.count[k] = count[b0 + k]; A.node[k] = node[b0 + k]; }
+        k_seg_sums<<<1, 64, 0, s>>>(A, out);
+        BIC_LAUNCHED();
     }
     return BICADMM_OK;
 }

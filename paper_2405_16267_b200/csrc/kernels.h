@@ -95,7 +95,9 @@ struct BlockVec {       // one local block's slice of the n*C vectors
 int launch_wsum(int64_t len, int64_t stride, const double* x_all, const double* u_all, int n_local_nodes, double* wsum,
                 cudaStream_t s);
 // u_ij += x_ij - z_j and per-CTA partials of ||x_ij - z_j||^2.
-int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s);
+int launch_u_update(BlockVec* bv, int nb, const double* z, double* partial, cudaStream_t s, int mode = 0);
+int launch_seg_sums(const double* const* ptr, const int64_t* count, const int32_t* node, int n, double* out,
+                    cudaStream_t s);
 // node_sq[i] = sum over local blocks of node i (blocks[] order) of partials.
 int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq,
                    cudaStream_t s);

@@ -156,3 +156,23 @@ def test_ls_refit_matches_oracle(bc, orc, M):
     xf = solver.get(bc.FIELD_X_FINAL)
     assert _rel(xf, ref["x_final"]) <= 1e-9
     assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
+
+
+def test_tol_mode_inner_loop_and_replay(bc, orc):
+    # DESIGN R7 / S:382: tolerance-mode inner loop on the GPU; its per-(outer, node)
+    # counts replayed by the oracle reproduce the GPU iterates to 1e-9, and agree
+    # with the oracle's own tolerance-mode counts (boundary flips are allowed but rare)
+    P = dg.generate(3, 300, 120, 6, "logistic", seed=21)
+    cs = dg.block_partition(120, 2)
+    K = 8
+    prm = dict(kappa=6, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=60, refit=0,
+               eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(**prm), cs)
+    solver.iterate(K)
+    counts = solver.get(bc.FIELD_INNER_COUNTS, np.int32).reshape(K, 3)
+    pb = orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs))
+    own = orc.run(pb, orc.Params(**prm))
+    rep = orc.run(pb, orc.Params(**prm), schedule=counts)
+    assert counts.min() >= 1 and counts.max() <= 60
+    assert _rel(solver.z, rep["z"]) <= 1e-9
+    assert np.mean(counts == own["inner_counts"]) >= 0.8
