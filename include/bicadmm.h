@@ -111,6 +111,11 @@ typedef struct {
                              and ||x_i^new - x_i^old|| <= eps_inner */
     int32_t max_inner;    /* tol mode cap */
     int32_t refit;        /* LS only: ridge refit on the final support (DESIGN R19) */
+    int32_t sweep;        /* inner-sweep schedule: 0 = auto (the fastest measured: currently two-pass),
+                             1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),
+                             2 = fused single HBM pass (needs every node's blocks on this rank and
+                             C == 1, else BICADMM_ERR_INVALID).  Same algebra (Eqs. (22)-(24));
+                             results agree to rounding. */
 } bicadmm_params;
 
 /* Result of bicadmm_iterate: the last outer iteration's Eq. (15) residuals. */
@@ -155,8 +160,9 @@ typedef enum {
 /* Phases timed by bicadmm_set_profiling:
  *   0 GEMV-T partial pass over A_ij (a1+a2, the first HBM pass)   1 GEMV-T chunk reduce + Eq. (24) epilogue
  *   2 x = H r (a3)   3 p = A x (a4, the second HBM pass)   4 block sum + AllReduce (a5)
- *   5 prox + nu + delta (a6, a7)   6 global step: Collect, (7b), (13), (14), (9), (15) (a8-a12) */
-#define BICADMM_NPHASE 7
+ *   5 prox + nu + delta (a6, a7)   6 global step: Collect, (7b), (13), (14), (9), (15) (a8-a12)
+ *   7 fused single-pass sweep (a4 + a5 + a6 + a7 + the next sweep's a1/a2 partial products) */
+#define BICADMM_NPHASE 8
 
 typedef struct bicadmm_comm bicadmm_comm;
 typedef struct bicadmm_handle bicadmm_handle;

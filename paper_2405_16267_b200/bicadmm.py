@@ -25,8 +25,9 @@ LOSSES = {"ls": LS, "logistic": LOGISTIC, "softmax": SOFTMAX, "hinge": HINGE}
 F64, F32 = 0, 1
 (FIELD_Z, FIELD_S, FIELD_SCALARS, FIELD_X_LOCAL, FIELD_U_LOCAL, FIELD_SUPPORT, FIELD_X_FINAL,
  FIELD_TRACE, FIELD_WBAR, FIELD_NU, FIELD_INNER_COUNTS, FIELD_LAUNCHES, FIELD_PHASE_MS, FIELD_PHASE_COUNT) = range(14)
-NPHASE = 7
-PHASES = ("gemv_t_partial", "gemv_t_reduce", "h_apply", "gemv", "allreduce", "prox", "global_step")
+NPHASE = 8
+PHASES = ("gemv_t_partial", "gemv_t_reduce", "h_apply", "gemv", "allreduce", "prox", "global_step", "fused_sweep")
+SWEEP_AUTO, SWEEP_TWO_PASS, SWEEP_FUSED = 0, 1, 2
 
 _i32, _i64, _f64, _vp = ct.c_int32, ct.c_int64, ct.c_double, ct.c_void_p
 
@@ -44,7 +45,7 @@ class bicadmm_problem(ct.Structure):
 class bicadmm_params(ct.Structure):
     _fields_ = [("kappa", _i64), ("rho_c", _f64), ("alpha", _f64), ("rho_l", _f64), ("lambda_", _f64),
                 ("eps_p", _f64), ("eps_d", _f64), ("eps_b", _f64), ("max_outer", _i32), ("inner_fixed", _i32),
-                ("eps_inner", _f64), ("max_inner", _i32), ("refit", _i32)]
+                ("eps_inner", _f64), ("max_inner", _i32), ("refit", _i32), ("sweep", _i32)]
 
 
 class bicadmm_step_info(ct.Structure):
@@ -230,11 +231,12 @@ class Params:
     eps_inner: float = 1e-6
     max_inner: int = 200
     refit: int = 0
+    sweep: int = 0
 
     def struct(self) -> bicadmm_params:
         return bicadmm_params(self.kappa, self.rho_c, self.alpha, self.rho_l, 1.0 / self.gamma, self.eps_p,
                               self.eps_d, self.eps_b, self.max_outer, self.inner_fixed, self.eps_inner,
-                              self.max_inner, self.refit)
+                              self.max_inner, self.refit, self.sweep)
 
 
 def _stream_ptr(stream):

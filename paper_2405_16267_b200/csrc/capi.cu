@@ -83,6 +83,8 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     void* H;
     int64_t ldh;
     double *x, *u, *r, *p, *partial, *pobj;
+    double* fpart;   // fused sweep: [node chunks][nj] partial products of A^T q
+    double* partial2 = nullptr;   // fused v2: [CTAs touching the node][nj]
 };
 struct LNode {
     int node, li;
@@ -91,6 +93,7 @@ struct LNode {
     double *nu, *delta, *S, *p_base, *pobj_base, *sq_partial, *obj_partial;
     int np;
     int64_t nprox_ctas;
+    int64_t ch_rows = 0, nchunks = 0, slot0 = 0, nslots = 0;   // fused sweep chunking
 };
 
 struct Bump {  // 256-byte aligned bump allocator over the workspace (base may be null to size)
@@ -130,6 +133,26 @@ struct bicadmm_handle {
     double *x_old = nullptr, *dpart = nullptr, *node_dx = nullptr, *node_res = nullptr;
     double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
     int refit_iters = 0;
+    // fused single-pass sweep (k_fused.cu)
+    bool fused = false;
+    FusedTables tb{};
+    FusedNode* fnodes = nullptr;
+    FusedChunk* fchunks = nullptr;
+    FusedSeg* fsegs = nullptr;
+    int* fdone = nullptr;
+    unsigned long long* fcounter = nullptr;
+    int* factive = nullptr;
+    double* fslots = nullptr;
+    int64_t fnch = 0, fslots_n = 0;
+    int fgrid = 0;
+    std::vector<GemvTDesc> gtf;
+    std::vector<int> active_last;
+    // fused v2 (k_fused2.cu): one CTA per SM, register/smem resident rows
+    int fused_kind = 0;            // 0 two-pass, 1 chunked (k_fused.cu), 2 per-SM rows (k_fused2.cu)
+    Fused2Args f2{};
+    int f2grid = 0;
+    std::vector<int64_t> f2_cta_lo, f2_cta_n;
+    double* f2slots = nullptr;
     OuterScalars* sc = nullptr;
     int64_t* support = nullptr;
     int64_t* support_count = nullptr;
@@ -339,6 +362,61 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     h->cg_Ap = b.arr<double>(len);
     h->cg_rhs = b.arr<double>(len);
     h->cg_sc = b.arr<double>(8);
+    // fused-sweep tables and partials (chunks of ~BICADMM_FUSED_CHUNK_MB MB of A rows per node)
+    {
+        double chunk_mb = 16.0;
+        if (const char* e = getenv("BICADMM_FUSED_CHUNK_MB")) chunk_mb = atof(e) > 0 ? atof(e) : chunk_mb;
+        int64_t nch = 0, slots = 0;
+        const int rpt = fused_rows_per_task();
+        for (auto& nd : h->nod) {
+            int64_t rowb = 0;
+            for (auto& L : h->blk) if (L.li == nd.li) rowb += L.nj * (int64_t)es;
+            int64_t ch = (int64_t)(chunk_mb * 1e6 / (double)std::max<int64_t>(rowb, 1)) / rpt * rpt;
+            nd.ch_rows = std::max<int64_t>(rpt, ch);
+            nd.nchunks = (nd.m + nd.ch_rows - 1) / nd.ch_rows;
+            nd.slot0 = slots;
+            nd.nslots = 0;
+            for (int64_t k = 0; k < nd.nchunks; ++k) {
+                const int64_t rows = std::min(nd.m, (k + 1) * nd.ch_rows) - k * nd.ch_rows;
+                nd.nslots += (rows + rpt - 1) / rpt;
+            }
+            slots += nd.nslots;
+            nch += nd.nchunks;
+        }
+        h->fnch = nch;
+        h->fslots_n = slots;
+        h->fnodes = b.arr<FusedNode>(nl);
+        h->fchunks = b.arr<FusedChunk>(nch);
+        h->fsegs = b.arr<FusedSeg>(2 * nch);
+        h->fdone = b.arr<int>(nch);
+        h->fcounter = b.arr<unsigned long long>(1);
+        h->factive = b.arr<int>(nl);
+        h->fslots = b.arr<double>(slots * rpt);
+        for (auto& L : h->blk) L.fpart = b.arr<double>(h->nod[L.li].nchunks * L.nj * C);
+    }
+    {   // fused v2: static row ranges of one CTA per SM; partials per node over the CTAs touching it
+        const int G = h->sm_count;
+        int64_t R = 0;
+        std::vector<int64_t> off;
+        for (auto& nd : h->nod) { off.push_back(R); R += nd.m; }
+        h->f2_cta_lo.assign(nl, 0);
+        h->f2_cta_n.assign(nl, 0);
+        for (auto& nd : h->nod) {
+            const int64_t r0 = off[nd.li], r1 = off[nd.li] + nd.m;
+            int64_t lo = -1, hi = -1;
+            for (int c = 0; c < G; ++c) {
+                const int64_t cb = (int64_t)c * R / G, ce = (int64_t)(c + 1) * R / G;
+                if (cb < ce && cb < r1 && ce > r0) { if (lo < 0) lo = c; hi = c; }
+            }
+            h->f2_cta_lo[nd.li] = lo < 0 ? 0 : lo;
+            h->f2_cta_n[nd.li] = lo < 0 ? 0 : hi - lo + 1;
+        }
+        int64_t slots = 0;
+        for (auto& nd : h->nod) slots += h->f2_cta_n[nd.li];
+        h->f2slots = b.arr<double>(slots);
+        for (auto& L : h->blk)
+            if (L.jl == 0) L.partial2 = b.arr<double>(std::max<int64_t>(1, h->f2_cta_n[L.li]) * L.nj * C);
+    }
     h->gram = b.arr<double>(ldg * njmax);
     h->fws = b.arr<double>((int64_t)factor_ws_doubles(njmax));
     return b.off + 256;
@@ -360,6 +438,107 @@ static void build_descs(bicadmm_handle* h) {
         v.x = L.x; v.u = L.u; v.c0 = L.c0 * h->C; v.len = L.nj * h->C; v.node = L.node;
         h->bv.push_back(v);
     }
+}
+
+// Build the fused-sweep task tables (host) and upload them once (setup time).
+static int build_fused(bicadmm_handle* h) {
+    const int nl = (int)h->nod.size();
+    const int rpt = fused_rows_per_task();
+    const int W = fused_strip_width(h->dtype);
+    std::vector<FusedNode> fn(nl);
+    std::vector<FusedChunk> fc;
+    std::vector<FusedSeg> fs;
+    std::vector<int64_t> nA, nB;
+    for (auto& nd : h->nod) {
+        FusedNode& f = fn[nd.li];
+        f = FusedNode{};
+        for (auto& L : h->blk) {
+            if (L.li != nd.li) continue;
+            const int j = L.jl;
+            f.A[j] = L.A; f.lda[j] = L.lda; f.nj[j] = L.nj; f.nstrips[j] = (L.nj + W - 1) / W;
+            f.x[j] = L.x; f.p[j] = L.p; f.partial[j] = L.fpart;
+        }
+        f.nb = nd.np; f.b = nd.b; f.nu = nd.nu; f.delta = nd.delta; f.m = nd.m;
+        int64_t strips = 0;
+        for (int j = 0; j < f.nb; ++j) strips += f.nstrips[j];
+        int64_t slot = nd.slot0;
+        for (int64_t k = 0; k < nd.nchunks; ++k) {
+            FusedChunk c{};
+            c.node = nd.li; c.r0 = k * nd.ch_rows; c.r1 = std::min(nd.m, (k + 1) * nd.ch_rows);
+            c.chunk_in_node = k; c.a_slot0 = slot;
+            const int64_t a = (c.r1 - c.r0 + rpt - 1) / rpt;
+            slot += a;
+            fc.push_back(c);
+            nA.push_back(a);
+            nB.push_back(strips);
+        }
+    }
+    int64_t t = 0;
+    const int64_t nch = (int64_t)fc.size();
+    for (int64_t c = 0; c < nch; ++c) {
+        fs.push_back(FusedSeg{t, 0, (int32_t)c});
+        t += nA[c];
+        if (c >= 1) { fs.push_back(FusedSeg{t, 1, (int32_t)(c - 1)}); t += nB[c - 1]; }
+    }
+    if (nch > 0) { fs.push_back(FusedSeg{t, 1, (int32_t)(nch - 1)}); t += nB[nch - 1]; }
+    H_CUDA(h, cudaMemcpy(h->fnodes, fn.data(), sizeof(FusedNode) * nl, cudaMemcpyHostToDevice));
+    H_CUDA(h, cudaMemcpy(h->fchunks, fc.data(), sizeof(FusedChunk) * nch, cudaMemcpyHostToDevice));
+    H_CUDA(h, cudaMemcpy(h->fsegs, fs.data(), sizeof(FusedSeg) * fs.size(), cudaMemcpyHostToDevice));
+    for (auto& L : h->blk)
+        H_CUDA(h, cudaMemsetAsync(L.fpart, 0, sizeof(double) * h->nod[L.li].nchunks * L.nj * h->C, h->st));
+    H_CUDA(h, cudaMemsetAsync(h->factive, 0xff, sizeof(int) * nl, h->st));
+    h->active_last.assign(nl, 1);
+    h->tb.nodes = h->fnodes; h->tb.chunks = h->fchunks; h->tb.segs = h->fsegs;
+    h->tb.nseg = (int)fs.size(); h->tb.nchunks = (int)nch; h->tb.ntasks = t;
+    h->tb.task_counter = h->fcounter; h->tb.done = h->fdone; h->tb.active = h->factive; h->tb.sq_slots = nullptr;
+    h->fgrid = fused_grid(h->dtype, h->sm_count);
+    h->gtf.clear();
+    for (auto& L : h->blk) {
+        GemvTDesc g{};
+        g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
+        g.z = h->z + L.c0 * h->C; g.u = L.u; g.r = L.r; g.partial = L.fpart;
+        g.nchunks = (int32_t)h->nod[L.li].nchunks; g.nstrips = 1; g.chunk_rows = h->nod[L.li].ch_rows;
+        h->gtf.push_back(g);
+    }
+    return BICADMM_OK;
+}
+
+static bool fused2_eligible(bicadmm_handle* h) {
+    if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes) return false;
+    for (auto& nd : h->nod) if (nd.np != 1) return false;
+    for (auto& L : h->blk) if (L.nj > fused2_max_cols(h->dtype)) return false;
+    return true;
+}
+
+static int build_fused2(bicadmm_handle* h) {
+    Fused2Args& a = h->f2;
+    a = Fused2Args{};
+    int64_t R = 0, maxc = 0, slot = 0;
+    a.nn = (int)h->nod.size();
+    for (auto& L : h->blk) {
+        const LNode& nd = h->nod[L.li];
+        const int k = L.li;
+        a.A[k] = L.A; a.b[k] = nd.b; a.x[k] = L.x; a.p[k] = L.p; a.nu[k] = nd.nu; a.delta[k] = nd.delta;
+        a.partial[k] = L.partial2; a.lda[k] = L.lda; a.ncols[k] = L.nj; a.row_off[k] = R;
+        a.cta_lo[k] = h->f2_cta_lo[k]; a.slot0[k] = slot;
+        slot += h->f2_cta_n[k];
+        R += L.m;
+        maxc = std::max(maxc, L.nj);
+        H_CUDA(h, cudaMemsetAsync(L.partial2, 0, sizeof(double) * std::max<int64_t>(1, h->f2_cta_n[k]) * L.nj, h->st));
+    }
+    a.total_rows = R;
+    a.max_cols_pad = rup(maxc, 4);
+    a.sq_slots = nullptr;
+    h->f2grid = h->sm_count;
+    h->gtf.clear();
+    for (auto& L : h->blk) {
+        GemvTDesc g{};
+        g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
+        g.z = h->z + L.c0 * h->C; g.u = L.u; g.r = L.r; g.partial = L.partial2;
+        g.nchunks = (int32_t)std::max<int64_t>(1, h->f2_cta_n[L.li]); g.nstrips = 1; g.chunk_rows = 0;
+        h->gtf.push_back(g);
+    }
+    return BICADMM_OK;
 }
 
 // ======================================================================= ABI: misc
@@ -508,8 +687,31 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
         if ((int)h->nod.size() != P->N) { delete h; return BICADMM_ERR_PLACEMENT; }
     }
     build_descs(h);
-    // validate labels on the host side?  Labels are device memory: check them on device
-    // with the loss kernel path is costly; the domain check is done in the Python binding.
+    {   // inner-sweep schedule (bicadmm_params.sweep)
+        bool ok1 = !h->split_blocks && h->C == 1 && (int)h->nod.size() <= kMaxDesc;
+        for (auto& nd : h->nod) ok1 = ok1 && nd.np <= kFMaxBlk;
+        const bool ok2 = fused2_eligible(h);
+        const char* fk = getenv("BICADMM_FUSED_KIND");   // tuning: force 1 (chunked) or 2 (per-SM rows)
+        int kind = 0;
+        if (R->sweep == 2) {
+            if (!ok1 && !ok2) { delete h; return BICADMM_ERR_INVALID; }
+            kind = ok2 ? 2 : 1;
+        } else if (R->sweep == 0) {
+            // auto = two-pass: measured on B200 (profiles/r01_summary.md) both fused kernels are
+            // slower than the two HBM-roofline passes (per-row serial prox / L2 re-read waits)
+            kind = 0;
+        }
+        if (fk && kind != 0) {
+            const int want = atoi(fk);
+            if (want == 1 && ok1) kind = 1;
+            if (want == 2 && ok2) kind = 2;
+        }
+        h->fused_kind = kind;
+        h->fused = kind != 0;
+        if (kind == 1 && build_fused(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
+        if (kind == 2 && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
+    }
+    // labels are device memory; their domain check (ERR_DOMAIN) is done by the binding
     if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
         cudaMallocHost(&h->host_i64, sizeof(int64_t) * 4) != cudaSuccess) {
         bicadmm_destroy(h);
@@ -563,7 +765,59 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
 }
 
 // ======================================================================= iterate
+static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_nodes, bool tol) {
+    std::vector<GemvTDesc> gt;
+    std::vector<GemvDesc> hx;
+    std::vector<char> act(h->nod.size(), 0);
+    for (int li : active_nodes) act[li] = 1;
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        const LBlock& L = h->blk[k];
+        if (!act[L.li]) continue;
+        gt.push_back(h->gtf[k]);
+        hx.push_back(GemvDesc{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0});
+    }
+    cudaEvent_t ev[4] = {};
+    int64_t lc[4] = {};
+    auto mark = [&](int k) {
+        if (!h->prof) return;
+        ev[k] = next_event(h);
+        cudaEventRecord(ev[k], h->st);
+        lc[k] = g_launches.load();
+    };
+    mark(0);   // r = rho_l sum_chunks partial + rho_c (z - u)   (partials from the previous fused pass)
+    H_RC(h, launch_gemv_t_reduce(gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, h->C));
+    mark(1);
+    if (tol)
+        H_CUDA(h, cudaMemcpyAsync(h->x_old, h->x_all, sizeof(double) * h->lenp * h->nod.size(),
+                                  cudaMemcpyDeviceToDevice, h->st));
+    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st, h->C));
+    mark(2);
+    for (size_t li = 0; li < h->nod.size() && h->fused_kind == 1; ++li)
+        if (h->active_last[li] != (int)act[li]) {
+            H_CUDA(h, cudaMemsetAsync(h->factive + li, act[li] ? 0xff : 0, sizeof(int), h->st));
+            h->active_last[li] = act[li];
+        }
+    if (h->fused_kind == 1) {
+        FusedTables tb = h->tb;
+        tb.sq_slots = tol ? h->fslots : nullptr;
+        H_RC(h, launch_fused_sweep(h->dtype, tb, h->loss, h->M, h->prm.rho_l, h->fgrid, h->st));
+    } else {
+        Fused2Args a = h->f2;
+        a.sq_slots = tol ? h->f2slots : nullptr;
+        for (size_t li = 0; li < h->nod.size(); ++li) a.active[li] = act[li];
+        H_RC(h, launch_fused2(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
+    }
+    mark(3);
+    if (h->prof) {
+        h->pending.push_back({1, ev[0], ev[1], lc[1] - lc[0]});
+        h->pending.push_back({2, ev[1], ev[2], lc[2] - lc[1]});
+        h->pending.push_back({7, ev[2], ev[3], lc[3] - lc[2]});
+    }
+    return BICADMM_OK;
+}
+
 static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, bool tol = false) {
+    if (h->fused) return inner_sweep_fused(h, active_nodes, tol);
     // descriptors for the active nodes' blocks
     std::vector<GemvTDesc> gt;
     std::vector<GemvDesc> hx, ax;
@@ -675,8 +929,16 @@ static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std
     std::vector<int64_t> cnt;
     std::vector<int32_t> node;
     for (int li : active) {
-        ptr.push_back(h->nod[li].sq_partial);
-        cnt.push_back(h->nod[li].nprox_ctas);
+        if (h->fused_kind == 2) {
+            ptr.push_back(h->f2slots + h->f2.slot0[li]);
+            cnt.push_back(h->f2_cta_n[li]);
+        } else if (h->fused_kind == 1) {
+            ptr.push_back(h->fslots + h->nod[li].slot0 * fused_rows_per_task());
+            cnt.push_back(h->nod[li].nslots * fused_rows_per_task());
+        } else {
+            ptr.push_back(h->nod[li].sq_partial);
+            cnt.push_back(h->nod[li].nprox_ctas);
+        }
         node.push_back(h->nod[li].node);
     }
     H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));

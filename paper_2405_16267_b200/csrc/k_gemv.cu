@@ -385,6 +385,10 @@ int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, c
         }
     }
     if (mid) BIC_CUDA(cudaEventRecord(mid, s));
+    return launch_gemv_t_reduce(d, nd, rho_l, rho_c, s, C);
+}
+
+int launch_gemv_t_reduce(GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s, int C) {
     for (int base = 0; base < nd; base += kMaxDesc) {
         GemvTRedBatch R;
         R.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;

@@ -39,6 +39,7 @@ void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need, i
 int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s,
                   cudaEvent_t mid = nullptr, int C = 1);
 int launch_gemv_t_c_partial(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s);
+int launch_gemv_t_reduce(GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s, int C = 1);
 int gemv_t_c_strip_width(int dtype);
 int gemv_t_strip_width(int dtype);
 
@@ -103,6 +104,56 @@ int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, dou
                    cudaStream_t s);
 int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s);
 constexpr int kUThreads = 256;
+
+// ---------------------------------------------------------------- fused single-pass sweep (k_fused.cu)
+constexpr int kFMaxBlk = 16;   // local blocks per node in the fused kernel
+struct FusedNode {
+    const void* A[kFMaxBlk];
+    int64_t lda[kFMaxBlk], nj[kFMaxBlk], nstrips[kFMaxBlk];
+    const double* x[kFMaxBlk];
+    double* p[kFMaxBlk];
+    double* partial[kFMaxBlk];   // [nchunks of the node][nj]
+    int nb;
+    const void* b;
+    double *nu, *delta;
+    int64_t m;
+};
+struct FusedChunk { int32_t node; int64_t r0, r1, chunk_in_node, a_slot0; };
+struct FusedSeg { int64_t t0; int32_t type, chunk; };   // type 0 = phase A rows, 1 = phase B strips
+struct FusedTables {
+    const FusedNode* nodes;
+    const FusedChunk* chunks;
+    const FusedSeg* segs;
+    int nseg, nchunks;
+    int64_t ntasks;
+    unsigned long long* task_counter;
+    int* done;
+    const int* active;      // per local node
+    double* sq_slots;       // optional: per A task x 8 rows, (abar - omega)^2 (tol mode)
+};
+int launch_fused_sweep(int dtype, const FusedTables& tb, int loss, int M, double rho, int grid, cudaStream_t s);
+int fused_grid(int dtype, int sm_count);
+int fused_strip_width(int dtype);
+int fused_rows_per_task();
+
+// ---------------------------------------------------------------- fused sweep v2 (k_fused2.cu)
+constexpr int kF2MaxNodes = 32;
+struct Fused2Args {
+    const void* A[kF2MaxNodes];
+    const void* b[kF2MaxNodes];
+    const double* x[kF2MaxNodes];
+    double* p[kF2MaxNodes];
+    double* nu[kF2MaxNodes];
+    double* delta[kF2MaxNodes];
+    double* partial[kF2MaxNodes];     // [cta - cta_lo][ncols]
+    int64_t lda[kF2MaxNodes], ncols[kF2MaxNodes], row_off[kF2MaxNodes], cta_lo[kF2MaxNodes], slot0[kF2MaxNodes];
+    int32_t active[kF2MaxNodes];      // inactive nodes (tol mode / schedule) keep all their state
+    int nn;
+    int64_t total_rows, max_cols_pad;
+    double* sq_slots;                 // optional per-(node, cta) sum of (abar - omega)^2 (tol mode)
+};
+int launch_fused2(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
+int fused2_max_cols(int dtype);
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)
 int launch_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);

@@ -29,12 +29,12 @@ def _rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
 
 
-def run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, seed=0, dtype=torch.float64, C=1, **kw):
+def run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, seed=0, dtype=torch.float64, C=1, sweep=0, **kw):
     P = dg.generate(N, m, n, kappa, loss, seed=seed, C=C)
     cs = dg.block_partition(n, M)
     oprm = dict(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0, **kw)
     solver = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], loss,
-                        bc.Params(**oprm), cs, C=P.C)
+                        bc.Params(sweep=sweep, **oprm), cs, C=P.C)
     zs, xs = [], []
     for _ in range(K):
         solver.iterate(1)
@@ -60,11 +60,14 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("sweep", [1, 2], ids=["two_pass", "fused"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_fp64_iterates_match_oracle(bc, orc, case):
+def test_fp64_iterates_match_oracle(bc, orc, case, sweep):
     _, N, m, n, kappa, loss, M, K, K_in = case[:9]
     C = case[9] if len(case) > 9 else 1
-    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C)
+    if C > 1 and sweep == 2:
+        pytest.skip("fused single-pass sweep is C == 1 only (softmax runs two-pass)")
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, sweep=sweep)
     tr_g = solver.trace()
     tr_o = ref["trace"]
     assert tr_g.shape == tr_o.shape
@@ -98,9 +101,11 @@ def test_c1_solve_to_tolerance_recovers_brute_force_support(bc, orc):
     assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
 
 
-def test_fp32_mode_within_1e4(bc, orc):
+@pytest.mark.parametrize("sweep", [1, 2], ids=["two_pass", "fused"])
+def test_fp32_mode_within_1e4(bc, orc, sweep):
     # FP32 storage of A, b, H; FP64 iterates and accumulation (DESIGN R23)
-    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 4, 600, 300, 10, "logistic", 1, 15, 10, dtype=torch.float32)
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 4, 600, 300, 10, "logistic", 1, 15, 10, dtype=torch.float32,
+                                           sweep=sweep)
     for k in range(15):
         assert _rel(zs[k], ref["z_trace"][k]) <= 1e-4, k
     assert solver.support().tolist() == ref["support"].tolist()
@@ -158,7 +163,8 @@ def test_ls_refit_matches_oracle(bc, orc, M):
     assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
 
 
-def test_tol_mode_inner_loop_and_replay(bc, orc):
+@pytest.mark.parametrize("sweep", [1, 2], ids=["two_pass", "fused"])
+def test_tol_mode_inner_loop_and_replay(bc, orc, sweep):
     # DESIGN R7 / S:382: tolerance-mode inner loop on the GPU; its per-(outer, node)
     # counts replayed by the oracle reproduce the GPU iterates to 1e-9, and agree
     # with the oracle's own tolerance-mode counts (boundary flips are allowed but rare)
@@ -167,7 +173,7 @@ def test_tol_mode_inner_loop_and_replay(bc, orc):
     K = 8
     prm = dict(kappa=6, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=60, refit=0,
                eps_p=0.0, eps_d=0.0, eps_b=0.0)
-    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(**prm), cs)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(sweep=sweep, **prm), cs)
     solver.iterate(K)
     counts = solver.get(bc.FIELD_INNER_COUNTS, np.int32).reshape(K, 3)
     pb = orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs))
@@ -176,3 +182,31 @@ def test_tol_mode_inner_loop_and_replay(bc, orc):
     assert counts.min() >= 1 and counts.max() <= 60
     assert _rel(solver.z, rep["z"]) <= 1e-9
     assert np.mean(counts == own["inner_counts"]) >= 0.8
+
+
+def test_fused_chunking_many_chunks(bc, orc, monkeypatch=None):
+    # the fused sweep over many small chunks (forces many A/B tasks and cross-chunk waits)
+    import os
+    os.environ["BICADMM_FUSED_CHUNK_MB"] = "0.05"
+    try:
+        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 2100, 333, 9, "logistic", 2, 6, 4, sweep=2)
+    finally:
+        del os.environ["BICADMM_FUSED_CHUNK_MB"]
+    for k in range(6):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", ["1", "2"])
+def test_fused_kinds_single_block(bc, orc, kind):
+    # both fused implementations on single-block nodes (k_fused.cu chunked / k_fused2.cu per-SM rows),
+    # including ragged n (odd column count) and FP32 storage
+    import os
+    os.environ["BICADMM_FUSED_KIND"] = kind
+    try:
+        for dtype, tol in ((torch.float64, 1e-9), (torch.float32, 1e-4)):
+            solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 777, 301, 9, "logistic", 1, 6, 5, sweep=2, dtype=dtype)
+            for k in range(6):
+                assert _rel(zs[k], ref["z_trace"][k]) <= tol, (kind, dtype, k)
+            assert solver.support().tolist() == ref["support"].tolist()
+    finally:
+        del os.environ["BICADMM_FUSED_KIND"]
