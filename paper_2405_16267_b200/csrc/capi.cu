@@ -90,7 +90,7 @@ struct LNode {
     int node, li;
     int64_t m;
     const void* b;
-    double *nu, *delta, *S, *p_base, *pobj_base, *sq_partial, *obj_partial;
+    double *nu, *delta, *S, *p_base, *pobj_base, *sq_partial, *obj_partial, *obar;
     int np;
     int64_t nprox_ctas;
     int64_t ch_rows = 0, nchunks = 0, slot0 = 0, nslots = 0;   // fused sweep chunking
@@ -330,6 +330,7 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         nd.nu = b.arr<double>(nd.m * C);
         nd.delta = b.arr<double>(nd.m * C);
         nd.S = b.arr<double>(nd.m * C);
+        nd.obar = b.arr<double>(nd.m * C);
         nd.p_base = b.arr<double>(nd.m * C * nd.np);
         nd.pobj_base = b.arr<double>(nd.m * C * nd.np);
         nd.nprox_ctas = (nd.m + kProxThreads - 1) / kProxThreads;
@@ -503,10 +504,11 @@ static int build_fused(bicadmm_handle* h) {
     return BICADMM_OK;
 }
 
-static bool fused2_eligible(bicadmm_handle* h) {
+static bool fused2_eligible(bicadmm_handle* h, int kind = 2) {
     if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes) return false;
     for (auto& nd : h->nod) if (nd.np != 1) return false;
-    for (auto& L : h->blk) if (L.nj > fused2_max_cols(h->dtype)) return false;
+    const int64_t cap = kind == 3 ? fused3_max_cols(h->dtype) : fused2_max_cols(h->dtype);
+    for (auto& L : h->blk) if (L.nj > cap) return false;
     return true;
 }
 
@@ -691,11 +693,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
         bool ok1 = !h->split_blocks && h->C == 1 && (int)h->nod.size() <= kMaxDesc;
         for (auto& nd : h->nod) ok1 = ok1 && nd.np <= kFMaxBlk;
         const bool ok2 = fused2_eligible(h);
+        const bool ok3 = fused2_eligible(h, 3);
         const char* fk = getenv("BICADMM_FUSED_KIND");   // tuning: force 1 (chunked) or 2 (per-SM rows)
         int kind = 0;
         if (R->sweep == 2) {
-            if (!ok1 && !ok2) { delete h; return BICADMM_ERR_INVALID; }
-            kind = ok2 ? 2 : 1;
+            if (!ok1 && !ok2 && !ok3) { delete h; return BICADMM_ERR_INVALID; }
+            kind = ok3 ? 3 : ok2 ? 2 : 1;
         } else if (R->sweep == 0) {
             // auto = two-pass: measured on B200 (profiles/r01_summary.md) both fused kernels are
             // slower than the two HBM-roofline passes (per-row serial prox / L2 re-read waits)
@@ -705,11 +708,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             const int want = atoi(fk);
             if (want == 1 && ok1) kind = 1;
             if (want == 2 && ok2) kind = 2;
+            if (want == 3 && ok3) kind = 3;
         }
         h->fused_kind = kind;
         h->fused = kind != 0;
         if (kind == 1 && build_fused(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
-        if (kind == 2 && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
+        if ((kind == 2 || kind == 3) && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
     }
     // labels are device memory; their domain check (ERR_DOMAIN) is done by the binding
     if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
@@ -734,7 +738,8 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     }
     for (auto& nd : h->nod) {
         if (zero(nd.nu, sizeof(double) * nd.m * C) || zero(nd.delta, sizeof(double) * nd.m * C) ||
-            zero(nd.p_base, sizeof(double) * nd.m * C * nd.np) || zero(nd.S, sizeof(double) * nd.m * C)) {
+            zero(nd.p_base, sizeof(double) * nd.m * C * nd.np) || zero(nd.S, sizeof(double) * nd.m * C) ||
+            zero(nd.obar, sizeof(double) * nd.m * C)) {
             bicadmm_destroy(h);
             return BICADMM_ERR_CUDA;
         }
@@ -804,8 +809,12 @@ static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_n
     } else {
         Fused2Args a = h->f2;
         a.sq_slots = tol ? h->f2slots : nullptr;
-        for (size_t li = 0; li < h->nod.size(); ++li) a.active[li] = act[li];
-        H_RC(h, launch_fused2(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
+        for (size_t li = 0; li < h->nod.size(); ++li) {
+            a.active[li] = act[li];
+            a.e2row[li] = tol ? h->nod[li].S : nullptr;   // S is unused on the single-rank fused path
+        }
+        if (h->fused_kind == 3) H_RC(h, launch_fused3(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
+        else H_RC(h, launch_fused2(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
     }
     mark(3);
     if (h->prof) {
@@ -837,7 +846,7 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
         const LNode& nd = h->nod[li];
         ProxNode p{};
         p.b = nd.b; p.p = nd.p_base; p.S = h->split_blocks ? nd.S : nullptr; p.nu = nd.nu; p.delta = nd.delta;
-        p.omega = nullptr; p.sq_partial = tol ? nd.sq_partial : nullptr; p.m = nd.m; p.pstride = nd.m * h->C;
+        p.omega = nd.obar; p.sq_partial = tol ? nd.sq_partial : nullptr; p.m = nd.m; p.pstride = nd.m * h->C;
         p.np = nd.np;
         px.push_back(p);
     }
@@ -941,7 +950,11 @@ static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std
         }
         node.push_back(h->nod[li].node);
     }
-    H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));
+    if (h->fused_kind == 3) {
+        for (int li : active) H_RC(h, launch_sum(h->nod[li].m, h->nod[li].S, h->node_res + h->nod[li].node, h->st));
+    } else {
+        H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));
+    }
     res.assign(h->N, 0.0);
     dx.assign(h->N, 0.0);
     H_CUDA(h, cudaMemcpyAsync(res.data(), h->node_res, sizeof(double) * h->N, cudaMemcpyDeviceToHost, h->st));

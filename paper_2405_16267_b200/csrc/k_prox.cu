@@ -30,9 +30,11 @@ __device__ __forceinline__ double sigmoid(double a) {
     return e / (1.0 + e);
 }
 
-__device__ __forceinline__ double prox_logistic(int M, double rho, double b, double p) {
-    // root of g(w) = -b sigma(-b M w) + rho (w - p), g' = M sigma (1 - sigma) + rho > 0
-    double lo = p - 1.0 / rho, hi = p + 1.0 / rho, w = p;
+__device__ __forceinline__ double prox_logistic(int M, double rho, double b, double p, double w0) {
+    // root of g(w) = -b sigma(-b M w) + rho (w - p), g' = M sigma (1 - sigma) + rho > 0;
+    // Newton from w0 (the previous sweep's omega of this sample, same root) when inside the bracket
+    double lo = p - 1.0 / rho, hi = p + 1.0 / rho;
+    double w = (w0 > lo && w0 < hi) ? w0 : p;
     const double Md = (double)M;
     for (int it = 0; it < 60; ++it) {
         const double sg = sigmoid(-b * Md * w);
@@ -133,7 +135,9 @@ __global__ void __launch_bounds__(kProxThreads) k_prox(const __grid_constant__ P
         if constexpr (LOSS == BICADMM_LS) {
             om[0] = (2.0 * bl + rho * pa[0]) / (2.0 * Md + rho);
         } else if constexpr (LOSS == BICADMM_LOGISTIC) {
-            om[0] = prox_logistic(M, rho, bl, pa[0]);
+            // Newton warm start: the previous sweep's omega of this sample (P.omega holds it)
+            const double w0 = P.omega ? P.omega[r] : pa[0];
+            om[0] = prox_logistic(M, rho, bl, pa[0], w0);
         } else if constexpr (LOSS == BICADMM_HINGE) {
             om[0] = prox_hinge(M, rho, bl, pa[0]);
         } else {

@@ -27,6 +27,20 @@ int launch_dot(int64_t n, const double* a, const double* b, double* out, cudaStr
     return BICADMM_OK;
 }
 
+__global__ void __launch_bounds__(1024) k_sum(int64_t n, const double* __restrict__ a, double* out) {
+    __shared__ double scratch[32];
+    double s = 0.0;
+    for (int64_t l = threadIdx.x; l < n; l += 1024) s += a[l];
+    s = block_sum(s, scratch);
+    if (threadIdx.x == 0) *out = s;
+}
+
+int launch_sum(int64_t n, const double* a, double* out, cudaStream_t s) {
+    k_sum<<<1, 1024, 0, s>>>(n, a, out);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
 // y[l] = mask[l] * (y[l] + lambda * v[l])
 __global__ void k_ridge_mask(int64_t n, const double* __restrict__ mask, const double* __restrict__ v, double lambda,
                              double* __restrict__ y) {

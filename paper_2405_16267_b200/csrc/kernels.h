@@ -148,15 +148,19 @@ struct Fused2Args {
     double* partial[kF2MaxNodes];     // [cta - cta_lo][ncols]
     int64_t lda[kF2MaxNodes], ncols[kF2MaxNodes], row_off[kF2MaxNodes], cta_lo[kF2MaxNodes], slot0[kF2MaxNodes];
     int32_t active[kF2MaxNodes];      // inactive nodes (tol mode / schedule) keep all their state
+    double* e2row[kF2MaxNodes];       // fused v3, tol mode: per-row (abar - omega)^2 (else null)
     int nn;
     int64_t total_rows, max_cols_pad;
     double* sq_slots;                 // optional per-(node, cta) sum of (abar - omega)^2 (tol mode)
 };
 int launch_fused2(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int fused2_max_cols(int dtype);
+int launch_fused3(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
+int fused3_max_cols(int dtype);
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)
 int launch_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
+int launch_sum(int64_t n, const double* a, double* out, cudaStream_t s);   // fixed-order single-CTA sum
 int launch_ridge_mask(int64_t n, const double* mask, const double* v, double lambda, double* y, cudaStream_t s);
 int launch_cg_xr(int64_t n, const double* sc, const double* p, const double* Ap, double* x, double* r, cudaStream_t s);
 int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStream_t s);

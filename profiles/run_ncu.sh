@@ -4,7 +4,7 @@
 set -u
 OUT=${1:-gpurun_out}
 mkdir -p "$OUT"
-CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
+CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-ttt"
 KREGEX='regex:k_gemv|k_prox|k_zt|k_s_update|k_u_update|k_node_sq|k_residuals|k_wsum'
 $CMD > "$OUT/plain.log" 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KREGEX" --csv \

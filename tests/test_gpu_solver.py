@@ -196,7 +196,7 @@ def test_fused_chunking_many_chunks(bc, orc, monkeypatch=None):
         assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9
 
 
-@pytest.mark.parametrize("kind", ["1", "2"])
+@pytest.mark.parametrize("kind", ["1", "2", "3"])
 def test_fused_kinds_single_block(bc, orc, kind):
     # both fused implementations on single-block nodes (k_fused.cu chunked / k_fused2.cu per-SM rows),
     # including ragged n (odd column count) and FP32 storage
