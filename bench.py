@@ -59,7 +59,31 @@ def parse():
     ap.add_argument("--cpu-n", type=int, default=1_000, help="cpu_baseline sample columns")
     ap.add_argument("--sweep", type=int, default=0, help="0 auto (fused single pass), 1 two-pass, 2 fused")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance row")
-    return ap.parse_args()
+    ap.add_argument("--config", default="C2", choices=sorted(PRESETS),
+                    help="BASELINE.json config preset (per-rank shape); C2 = configs[1] (default)")
+    a = ap.parse_args()
+    pr = PRESETS[a.config]
+    for k, v in pr.items():
+        if k != "workload":
+            setattr(a, k, v)
+    a.workload = pr["workload"]
+    return a
+
+
+# Per-rank shapes of BASELINE.json configs that fit one B200.
+PRESETS = {
+    "C2": dict(nodes=4, m=25_000, n=10_000, kappa=100, loss="logistic", C=1, M=1, inner=10, workload=WORKLOAD),
+    "C2ls": dict(nodes=4, m=25_000, n=10_000, kappa=100, loss="ls", C=1, M=1, inner=10,
+                 workload="configs[1] shape with the LS loss (diagnostic: closed-form prox)"),
+    "C1": dict(nodes=2, m=100, n=50, kappa=5, loss="ls", C=1, M=1, inner=10,
+               workload="configs[0]: sparse LS, N=2 nodes x m_i=100, n=50, kappa=5, M=1, FP64 (launch-bound)"),
+    "C4": dict(nodes=1, m=500_000, n=20_000, kappa=500, loss="softmax", C=10, M=8, inner=5,
+               workload="configs[3] at G=1: sparse softmax, C=10 classes, N=1 node x m=500k, n=20k, kappa=500, "
+                        "M=8 feature blocks on one GPU, FP64, K_in=5 (A = 80 GB)"),
+    "C3s": dict(nodes=1, m=1_000_000, n=12_500, kappa=125, loss="ls", C=1, M=1, inner=5,
+                workload="configs[2] per-GPU shard: sparse LS, m=1M rows x n_j=12.5k (one of the 8 feature blocks; "
+                         "the cross-GPU block-sum AllReduce is absent on one GPU), FP64, K_in=5 (A = 100 GB)"),
+}
 
 
 def measured_peaks():
@@ -159,9 +183,16 @@ def run_ours(args):
     dtype = torch.float64 if args.dtype == "f64" else torch.float32
     nl = args.nodes
     N = nl * world
-    n, m = args.n, args.m
-    cs = dg.block_partition(n, 1)
-    P = dg.generate(nl, m, n, args.kappa, args.loss, seed=1000 + rank, device="cuda", dtype=dtype)
+    n, m, C, M = args.n, args.m, args.C, args.M
+    cs = dg.block_partition(n, M)
+    P = dg.generate(nl, m, n, args.kappa, args.loss, C=C, seed=1000 + rank, device="cuda", dtype=dtype)
+    if n % 4:   # rows must start 16-byte aligned (lda % 4 == 0): pad the node matrices (configs[0])
+        padded = []
+        for a in P.A:
+            t = torch.zeros(a.shape[0], -(-n // 4) * 4, dtype=a.dtype, device=a.device)
+            t[:, :n] = a
+            padded.append(t)
+        P.A = padded
     comm = None
     if world > 1:
         uid = [bc.bicadmm_get_unique_id() if rank == 0 else None]
@@ -172,11 +203,12 @@ def run_ours(args):
     for k in range(nl):
         i = rank * nl + k
         b_all[i] = P.b[k]
-        blocks.append((i, 0, P.A[k]))
+        for j in range(M):
+            blocks.append((i, j, P.A[k][:, cs[j]:cs[j + 1]]))
     prm = bc.Params(kappa=args.kappa, max_outer=10 ** 6, inner_fixed=args.inner, refit=0,
                     eps_p=0.0, eps_d=0.0, eps_b=0.0, sweep=args.sweep)
     t0 = time.time()
-    solver = bc.BiCADMM(None, b_all, args.loss, prm, cs, blocks=blocks, comm=comm)
+    solver = bc.BiCADMM(None, b_all, args.loss, prm, cs, blocks=blocks, comm=comm, C=C)
     setup_wall = time.time() - t0
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -211,8 +243,9 @@ def run_ours(args):
     # roofline of the dominant kernel (an HBM pass over every local A_ij)
     s = 8 if args.dtype == "f64" else 4
     A_bytes = nl * m * n * s
-    byt = {"gemv": A_bytes + nl * (8 * n + 8 * m), "gemv_t_partial": A_bytes + nl * 16 * m,
-           "h_apply": nl * (n * n * s + 16 * n),
+    nj_list = [cs[j + 1] - cs[j] for j in range(M)]
+    byt = {"gemv": A_bytes + nl * 8 * C * (n + M * m), "gemv_t_partial": A_bytes + nl * 16 * C * m * M,
+           "h_apply": nl * sum(nj * nj * s + 16 * C * nj for nj in nj_list),
            # fused: A once from HBM (phase B re-reads it from L2) + x, b, p, nu, delta
            "fused_sweep": A_bytes + nl * (8 * n + s * m + 8 * 5 * m)}
     cand = {k: phases[k] for k in byt if phases[k][1] > 0}
@@ -255,8 +288,9 @@ def run_ours(args):
         blocks2 = []
         for k in range(nl):
             b_all2[rank * nl + k] = db[k]
-            blocks2.append((rank * nl + k, 0, dA[k]))
-        s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False)
+            for j in range(M):
+                blocks2.append((rank * nl + k, j, dA[k][:, cs[j]:cs[j + 1]]))
+        s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False, C=C)
         for _ in range(args.steps):
             s2.iterate(1)          # each step reads back its 6 residual scalars
         z = s2.z                   # D2H of the result
@@ -275,10 +309,10 @@ def run_ours(args):
         s2.close()
 
     ttt = None
-    if rank == 0 and world == 1 and not args.no_ttt:
+    if rank == 0 and world == 1 and not args.no_ttt and args.config == "C2":
         ttt = time_to_tol(bc, dg, np, torch, args.sweep)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "C2":
         o = oracle_sample(args.cpu_m, args.cpu_n, args.inner, 2, 1, n, m)
         cpu = {"value": o["value"] * N / nl if False else o["value"], "unit": UNIT, "cores": o["cores"],
                "kind": "oracle", "sample": o["sample"]}
@@ -288,8 +322,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded, P:268 recipe; DESIGN.md 5)",
-            "config": {"workload": WORKLOAD if (args.n, args.m, args.nodes, args.loss) == (10_000, 25_000, 4, "logistic")
-                       else f"custom: {args.loss}, {nl} nodes/rank x m_i={m}, n={n}, kappa={args.kappa}",
+            "config": {"workload": args.workload, "preset": args.config, "C": C, "M": M,
                        "nodes_total": N, "nodes_per_rank": nl, "m_i": m, "n": n, "kappa": args.kappa,
                        "K_in": args.inner, "placement": "node-major" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (A = %.1f GB/rank)" % (A_bytes / 1e9),

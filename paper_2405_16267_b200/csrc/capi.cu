@@ -85,6 +85,7 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     double *x, *u, *r, *p, *partial, *pobj;
     double* fpart;   // fused sweep: [node chunks][nj] partial products of A^T q
     double* partial2 = nullptr;   // fused v2: [CTAs touching the node][nj]
+    double* xt = nullptr;         // C > 1: class-major scratch (nj * C)
 };
 struct LNode {
     int node, li;
@@ -352,6 +353,7 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         L.u = h->u_all + (base ? (int64_t)L.li * lenp + L.c0 * C : 0);
         L.p = nd.p_base + (base ? (int64_t)L.jl * nd.m * C : 0);
         L.r = b.arr<double>(L.nj * C);
+        L.xt = C > 1 ? b.arr<double>(L.nj * C) : nullptr;
         L.pobj = nd.pobj_base + (base ? (int64_t)L.jl * nd.m * C : 0);
         L.partial = b.arr<double>(need[k]);
     }
@@ -507,8 +509,10 @@ static int build_fused(bicadmm_handle* h) {
 static bool fused2_eligible(bicadmm_handle* h, int kind = 2) {
     if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes) return false;
     for (auto& nd : h->nod) if (nd.np != 1) return false;
-    const int64_t cap = kind == 3 ? fused3_max_cols(h->dtype) : fused2_max_cols(h->dtype);
-    for (auto& L : h->blk) if (L.nj > cap) return false;
+    const int64_t cap = kind == 4 ? fused4_max_cols(h->dtype) : kind == 3 ? fused3_max_cols(h->dtype)
+                                                                            : fused2_max_cols(h->dtype);
+    for (auto& L : h->blk) if (L.nj > cap || (kind == 4 && L.nj % 8)) return false;
+    if (kind == 4 && h->sm_count < 2) return false;
     return true;
 }
 
@@ -516,6 +520,23 @@ static int build_fused2(bicadmm_handle* h) {
     Fused2Args& a = h->f2;
     a = Fused2Args{};
     int64_t R = 0, maxc = 0, slot = 0;
+    if (h->fused_kind == 4) {
+        // row ranges per CTA pair (cluster of 2): recompute the touching ranges with G/2 units
+        const int G = h->sm_count / 2;
+        int64_t tot = 0;
+        std::vector<int64_t> off;
+        for (auto& nd : h->nod) { off.push_back(tot); tot += nd.m; }
+        for (auto& nd : h->nod) {
+            const int64_t r0 = off[nd.li], r1 = off[nd.li] + nd.m;
+            int64_t lo = -1, hi = -1;
+            for (int c = 0; c < G; ++c) {
+                const int64_t cb = (int64_t)c * tot / G, ce = (int64_t)(c + 1) * tot / G;
+                if (cb < ce && cb < r1 && ce > r0) { if (lo < 0) lo = c; hi = c; }
+            }
+            h->f2_cta_lo[nd.li] = lo < 0 ? 0 : lo;
+            h->f2_cta_n[nd.li] = lo < 0 ? 0 : hi - lo + 1;
+        }
+    }
     a.nn = (int)h->nod.size();
     for (auto& L : h->blk) {
         const LNode& nd = h->nod[L.li];
@@ -531,7 +552,7 @@ static int build_fused2(bicadmm_handle* h) {
     a.total_rows = R;
     a.max_cols_pad = rup(maxc, 4);
     a.sq_slots = nullptr;
-    h->f2grid = h->sm_count;
+    h->f2grid = h->fused_kind == 4 ? (h->sm_count / 2) * 2 : h->sm_count;
     h->gtf.clear();
     for (auto& L : h->blk) {
         GemvTDesc g{};
@@ -694,11 +715,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
         for (auto& nd : h->nod) ok1 = ok1 && nd.np <= kFMaxBlk;
         const bool ok2 = fused2_eligible(h);
         const bool ok3 = fused2_eligible(h, 3);
+        const bool ok4 = fused2_eligible(h, 4);
         const char* fk = getenv("BICADMM_FUSED_KIND");   // tuning: force 1 (chunked) or 2 (per-SM rows)
         int kind = 0;
         if (R->sweep == 2) {
-            if (!ok1 && !ok2 && !ok3) { delete h; return BICADMM_ERR_INVALID; }
-            kind = ok3 ? 3 : ok2 ? 2 : 1;
+            if (!ok1 && !ok2 && !ok3 && !ok4) { delete h; return BICADMM_ERR_INVALID; }
+            kind = ok4 ? 4 : ok3 ? 3 : ok2 ? 2 : 1;
         } else if (R->sweep == 0) {
             // auto = two-pass: measured on B200 (profiles/r01_summary.md) both fused kernels are
             // slower than the two HBM-roofline passes (per-row serial prox / L2 re-read waits)
@@ -709,11 +731,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             if (want == 1 && ok1) kind = 1;
             if (want == 2 && ok2) kind = 2;
             if (want == 3 && ok3) kind = 3;
+            if (want == 4 && ok4) kind = 4;
         }
         h->fused_kind = kind;
         h->fused = kind != 0;
         if (kind == 1 && build_fused(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
-        if ((kind == 2 || kind == 3) && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
+        if (kind >= 2 && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
     }
     // labels are device memory; their domain check (ERR_DOMAIN) is done by the binding
     if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
@@ -813,7 +836,10 @@ static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_n
             a.active[li] = act[li];
             a.e2row[li] = tol ? h->nod[li].S : nullptr;   // S is unused on the single-rank fused path
         }
-        if (h->fused_kind == 3) H_RC(h, launch_fused3(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
+        static const bool fast_dbg = getenv("BICADMM_FUSED_DEBUG_LSPROX") != nullptr;   // timing experiments only
+        const int floss = fast_dbg ? BICADMM_LS : h->loss;
+        if (h->fused_kind == 4) H_RC(h, launch_fused4(h->dtype, a, floss, h->prm.rho_l, h->f2grid, h->st));
+        else if (h->fused_kind == 3) H_RC(h, launch_fused3(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
         else H_RC(h, launch_fused2(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
     }
     mark(3);
@@ -837,9 +863,9 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
         const LBlock& L = h->blk[k];
         if (!act[L.li]) continue;
         gt.push_back(h->gt[k]);
-        GemvDesc d1{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0};
+        GemvDesc d1{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0, L.xt};
         hx.push_back(d1);
-        GemvDesc d2{L.A, L.lda, L.m, L.nj, L.x, L.p, 0};
+        GemvDesc d2{L.A, L.lda, L.m, L.nj, L.x, L.p, 0, L.xt};
         ax.push_back(d2);
     }
     for (int li : active_nodes) {
@@ -950,7 +976,7 @@ static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std
         }
         node.push_back(h->nod[li].node);
     }
-    if (h->fused_kind == 3) {
+    if (h->fused_kind >= 3) {
         for (int li : active) H_RC(h, launch_sum(h->nod[li].m, h->nod[li].S, h->node_res + h->nod[li].node, h->st));
     } else {
         H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));
@@ -1138,7 +1164,7 @@ static int do_finalize(bicadmm_handle* h) {
     if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
-    for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0});
+    for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0, L.xt});
     H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, h->C));
     std::vector<ProxNode> px;
     for (auto& nd : h->nod) {

@@ -46,11 +46,13 @@ __device__ double f2_prox(int loss, double rho, double b, double p) {
         const double g = -b * sg + rho * (w - p);
         if (g > 0.0) hi = w; else lo = w;
         const double gp = sg * (1.0 - sg) + rho;
-        double wn = w - g / gp;
+        const double step = g / gp;
+        // converged: accept the Newton step (checked BEFORE the bracket safeguard, which
+        // would otherwise turn an ulp-sized step landing on the bracket into a bisection)
+        if (fabs(step) <= 4.0 * DBL_EPSILON * fmax(1.0, fabs(w))) { w -= step; break; }
+        double wn = w - step;
         if (!(wn > lo && wn < hi)) wn = 0.5 * (lo + hi);
-        const double step = fabs(wn - w);
         w = wn;
-        if (step <= 4.0 * DBL_EPSILON * fmax(1.0, fabs(w))) break;
     }
     return w;
 }

@@ -1,0 +1,344 @@
+// k_fused4.cu -- single-HBM-read inner sweep on CTA pairs.
+//
+// Same algebra as the two-pass sweep (Eqs. (22)-(24)) for nodes with one local
+// block.  A cluster of 2 CTAs (2 SMs) owns a contiguous row range; CTA h of the pair
+// owns column half h of every row, so a 4-deep ring of half-rows fits in shared
+// memory even at n = 10^4 in FP64 (4 x 40 KB):
+//
+//   producer warp : TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of half-row
+//                   k + 2 into the ring while rows k, k+1 are being used
+//   12 main warps : dot of half-row k with x (x half in registers) -> 12 partials
+//                   written to BOTH CTAs' smem (local st.shared + DSMEM st.shared::cluster)
+//                   with release arrives on both CTAs' "dot" mbarriers;
+//                   axpy acc[col] += A[k-2, col] q_{k-2} from the ring (no second read)
+//   3 prox warps  : wait for the 24 partials of a row, p = fixed-order sum (identical
+//                   in both CTAs), omega = prox(p + nu) (22), nu += p - omega (23),
+//                   delta = omega - p - nu, q = p + delta; rank 0 stores p, nu, delta.
+//
+// Both CTAs compute the prox redundantly from bit-identical inputs, so the only
+// cluster traffic per row is 12 doubles + one remote arrive each way.  A crosses
+// HBM exactly once per sweep; partial products are written per cluster and reduced
+// in fixed order by the next sweep's Eq. (24) epilogue (bit-reproducible).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bic {
+
+constexpr int kF4Main = 12;                    // main warps per CTA
+constexpr int kF4Prox = 3;                     // prox warps per CTA
+constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp = 512
+constexpr int kF4MainT = 32 * kF4Main;         // 384
+constexpr int kF4Ring = 4;                     // half-row ring
+constexpr int kF4D = 2;                        // axpy delay (rows)
+constexpr int kF4Q = 8;                        // dot / q slots (>= lag window, see below)
+
+__device__ __forceinline__ double f4_sigmoid(double a) {
+    if (a >= 0.0) return 1.0 / (1.0 + exp(-a));
+    const double e = exp(a);
+    return e / (1.0 + e);
+}
+
+__device__ double f4_prox(int loss, double rho, double b, double p, double w0) {
+    if (loss == BICADMM_LS) return (2.0 * b + rho * p) / (2.0 + rho);
+    if (loss == BICADMM_HINGE) {
+        const double pp = b * p;
+        double y;
+        if (pp > 1.0) y = pp;
+        else if (pp + 1.0 / rho < 1.0) y = pp + 1.0 / rho;
+        else y = 1.0;
+        return b * y;
+    }
+    double lo = p - 1.0 / rho, hi = p + 1.0 / rho;
+    double w = (w0 > lo && w0 < hi) ? w0 : p;
+    for (int it = 0; it < 60; ++it) {
+        const double sg = f4_sigmoid(-b * w);
+        const double g = -b * sg + rho * (w - p);
+        if (g > 0.0) hi = w; else lo = w;
+        const double gp = sg * (1.0 - sg) + rho;
+        const double step = g / gp;
+        // converged: accept the Newton step (checked BEFORE the bracket safeguard, which
+        // would otherwise turn an ulp-sized step landing on the bracket into a bisection)
+        if (fabs(step) <= 4.0 * DBL_EPSILON * fmax(1.0, fabs(w))) { w -= step; break; }
+        double wn = w - step;
+        if (!(wn > lo && wn < hi)) wn = 0.5 * (lo + hi);
+        w = wn;
+    }
+    return w;
+}
+
+// ---- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned mapa(unsigned local, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mb4_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mb4_arrive_local(uint64_t* b) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb4_arrive_remote(unsigned cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mb4_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// bounded waits: a protocol bug traps (error) instead of hanging the GPU
+__device__ __forceinline__ bool mb4_try_cta(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mb4_try_cluster(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mb4_wait_cta(uint64_t* b, unsigned parity) {
+    for (long long it = 0; !mb4_try_cta(b, parity); ++it)
+        if (it > (1ll << 26)) asm volatile("trap;");
+}
+__device__ __forceinline__ void mb4_wait_cluster(uint64_t* b, unsigned parity) {
+    for (long long it = 0; !mb4_try_cluster(b, parity); ++it)
+        if (it > (1ll << 26)) asm volatile("trap;");
+}
+__device__ __forceinline__ void st_cluster_f64(unsigned cluster_addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cluster_addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <typename T, int E>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
+    k_fused4(const Fused2Args a, int loss, double rho) {
+    extern __shared__ __align__(128) unsigned char f4_smem[];
+    T* ring = reinterpret_cast<T*>(f4_smem);             // kF4Ring x half_pad elements
+    __shared__ double dotp[kF4Q][2 * kF4Main];            // [slot][cta * 12 + warp]
+    __shared__ double qv[kF4Q];
+    __shared__ __align__(8) uint64_t bar_full[kF4Ring], bar_empty[kF4Ring], bar_dot[kF4Q], bar_q[kF4Q];
+    const unsigned h = cluster_rank();                     // column half owned by this CTA
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t clu = blockIdx.x >> 1, nclu = gridDim.x >> 1;
+    const int64_t rb = clu * a.total_rows / nclu, re = (clu + 1) * a.total_rows / nclu;
+    const int64_t half_pad = ((a.max_cols_pad / 2 + 3) / 4) * 4 + 4;   // elements per ring slot (>= ch)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kF4Ring; ++s) { mb4_init(&bar_full[s], 1); mb4_init(&bar_empty[s], kF4Main); }
+        for (int s = 0; s < kF4Q; ++s) { mb4_init(&bar_dot[s], 2 * kF4Main); mb4_init(&bar_q[s], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync_all();   // barriers of both CTAs initialised before any remote arrive
+    if (rb >= re) { cluster_sync_all(); return; }
+    auto node_of = [&](int64_t r, int from) {
+        int k = from;
+        while (k + 1 < a.nn && r >= a.row_off[k + 1]) ++k;
+        return k;
+    };
+    // column split of node nd (ncols % 8 == 0): half 0 = [0, ch), half 1 = [ch, ncols), ch % 4 == 0,
+    // so both halves start 16-byte aligned and are whole 16-byte multiples (TMA bulk copy)
+    auto half_range = [&](int nd, int64_t& c0, int64_t& cn) {
+        const int64_t nc = a.ncols[nd];
+        const int64_t ch = ((nc / 2 + 3) / 4) * 4;
+        c0 = h == 0 ? 0 : ch;
+        cn = h == 0 ? ch : nc - ch;
+    };
+    const int nd0 = node_of(rb, 0);
+
+    if (warp == kF4Main + kF4Prox) {
+        // ------------------------------------------------------------ producer (lane 0)
+        if (lane == 0) {
+            int nd = nd0;
+            for (int64_t r = rb; r < re; ++r) {
+                nd = node_of(r, nd);
+                const int s = (int)((r - rb) % kF4Ring);
+                const int64_t u = (r - rb) / kF4Ring;
+                if (u >= 1) mb4_wait_cta(&bar_empty[s], (unsigned)((u - 1) & 1));
+                int64_t c0, cn;
+                half_range(nd, c0, cn);
+                const unsigned bytes = (unsigned)(cn * (int64_t)sizeof(T));
+                mb4_expect_tx(&bar_full[s], bytes);
+                if (bytes)
+                    tma_bulk_g2s(ring + s * half_pad,
+                                 static_cast<const T*>(a.A[nd]) + (r - a.row_off[nd]) * a.lda[nd] + c0, bytes,
+                                 &bar_full[s]);
+            }
+        }
+    } else if (warp < kF4Main) {
+        // ------------------------------------------------------------ main warps
+        const int mt = threadIdx.x;
+        const unsigned peer = h ^ 1u;
+        int ndd = nd0, nda = nd0;
+        double xr[E], acc[E];
+        int64_t hc0, hcn;
+        auto load_x = [&](int nd) {
+            half_range(nd, hc0, hcn);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t c = mt + (int64_t)kF4MainT * e;
+                xr[e] = c < hcn ? a.x[nd][hc0 + c] : 0.0;
+            }
+        };
+        load_x(ndd);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.0;
+        int64_t ac0, acn;
+        half_range(nda, ac0, acn);
+        auto flush = [&](int node) {
+            double* out = a.partial[node] + (clu - a.cta_lo[node]) * a.ncols[node] + ac0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t c = mt + (int64_t)kF4MainT * e;
+                if (c < acn) out[c] = acc[e];
+                acc[e] = 0.0;
+            }
+        };
+        for (int64_t k = rb; k < re + kF4D; ++k) {
+            if (k < re) {
+                const int nn2 = node_of(k, ndd);
+                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
+                const int s = (int)((k - rb) % kF4Ring);
+                mb4_wait_cta(&bar_full[s], (unsigned)(((k - rb) / kF4Ring) & 1));
+                const T* row = ring + s * half_pad;
+                double dot = 0.0;
+                if (a.active[ndd]) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int64_t c = mt + (int64_t)kF4MainT * e;
+                        if (c < hcn) dot = fma((double)row[c], xr[e], dot);
+                    }
+                }
+                dot = warp_sum(dot);
+                if (lane == 0) {
+                    const int q = (int)((k - rb) % kF4Q);
+                    const int idx = (int)h * kF4Main + warp;
+                    dotp[q][idx] = dot;
+                    st_cluster_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot);
+                    mb4_arrive_local(&bar_dot[q]);
+                    mb4_arrive_remote(mapa(smem_u32(&bar_dot[q]), peer));
+                }
+            }
+            const int64_t ra = k - kF4D;
+            if (ra >= rb) {
+                const int nn2 = node_of(ra, nda);
+                if (nn2 != nda) {
+                    if (a.active[nda]) flush(nda);
+                    nda = nn2;
+                    half_range(nda, ac0, acn);
+                }
+                const int q = (int)((ra - rb) % kF4Q);
+                mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
+                const double qq = qv[q];
+                const int s = (int)((ra - rb) % kF4Ring);
+                const T* row = ring + s * half_pad;
+                if (a.active[nda]) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int64_t c = mt + (int64_t)kF4MainT * e;
+                        if (c < acn) acc[e] = fma((double)row[c], qq, acc[e]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mb4_arrive_local(&bar_empty[s]);
+            }
+        }
+        if (a.active[nda]) flush(nda);
+    } else if (lane == 0) {
+        // ------------------------------------------------------------ prox warps (lane 0)
+        const int pw = warp - kF4Main;
+        int nd = nd0;
+        for (int64_t r = rb + pw; r < re; r += kF4Prox) {
+            nd = node_of(r, nd);
+            const int q = (int)((r - rb) % kF4Q);
+            const int64_t rl = r - a.row_off[nd];
+            const bool on = a.active[nd];
+            double bl = 0.0, nu0 = 0.0, w0 = 0.0;
+            if (on) {
+                bl = (double)static_cast<const T*>(a.b[nd])[rl];
+                nu0 = a.nu[nd][rl];
+                w0 = a.delta[nd][rl] + a.p[nd][rl] + nu0;
+            }
+            mb4_wait_cluster(&bar_dot[q], (unsigned)(((r - rb) / kF4Q) & 1));
+            double qq = 0.0;
+            if (on) {
+                double p = 0.0;
+#pragma unroll
+                for (int w = 0; w < 2 * kF4Main; ++w) p += dotp[q][w];
+                const double om = f4_prox(loss, rho, bl, p + nu0, w0);
+                const double nu = nu0 + p - om;
+                const double dl = om - p - nu;
+                if (h == 0) {
+                    a.p[nd][rl] = p;
+                    a.nu[nd][rl] = nu;
+                    a.delta[nd][rl] = dl;
+                    if (a.e2row[nd]) a.e2row[nd][rl] = (p - om) * (p - om);
+                }
+                qq = p + dl;
+            }
+            qv[q] = qq;
+            mb4_arrive_local(&bar_q[q]);
+        }
+    }
+    cluster_sync_all();   // no CTA exits while its peer may still write into its smem
+}
+
+int fused4_max_cols(int dtype) { return dtype == BICADMM_F64 ? 2 * kF4MainT * 16 : 2 * kF4MainT * 16; }
+
+template <typename T>
+static int f4_launch(int E, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
+    const size_t smem = (size_t)kF4Ring * (((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * sizeof(T);
+#define F4_CASE(EE)                                                                                            \
+    case EE: {                                                                                                 \
+        static bool set = false;                                                                               \
+        if (!set) {                                                                                            \
+            if (cudaFuncSetAttribute(k_fused4<T, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != \
+                cudaSuccess)                                                                                   \
+                return BICADMM_ERR_CUDA;                                                                       \
+            set = true;                                                                                        \
+        }                                                                                                      \
+        k_fused4<T, EE><<<grid, kF4Threads, smem, s>>>(a, loss, rho);                                          \
+        break;                                                                                                 \
+    }
+    switch (E) {
+        F4_CASE(2) F4_CASE(4) F4_CASE(8) F4_CASE(12) F4_CASE(16)
+    default: return BICADMM_ERR_INVALID;
+    }
+#undef F4_CASE
+    return BICADMM_OK;
+}
+
+int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
+    int64_t maxc = 0;
+    for (int k = 0; k < a.nn; ++k) maxc = a.ncols[k] > maxc ? a.ncols[k] : maxc;
+    const int64_t half = (maxc + 1) / 2 + 2;
+    const int64_t e = (half + kF4MainT - 1) / kF4MainT;
+    const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 16 ? 16 : -1;
+    const size_t smem = (size_t)kF4Ring * (((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * (dtype == BICADMM_F64 ? 8 : 4);
+    if (E < 0 || smem > 200 * 1024 || (grid & 1)) return BICADMM_ERR_INVALID;
+    for (int k = 0; k < a.nn; ++k) if (a.ncols[k] % 8) return BICADMM_ERR_INVALID;
+    int rc = dtype == BICADMM_F64 ? f4_launch<double>(E, a, loss, rho, grid, s) : f4_launch<float>(E, a, loss, rho, grid, s);
+    if (rc) return rc;
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+}  // namespace bic

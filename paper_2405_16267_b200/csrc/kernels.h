@@ -14,6 +14,7 @@ struct GemvDesc {
     const double* x;
     double* y;
     int64_t task_begin;  // filled by the launcher
+    double* xt = nullptr;   // C > 1: scratch (cols * C) for the class-major copy of x
 };
 int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s, int C = 1);
 int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
@@ -156,6 +157,8 @@ struct Fused2Args {
 int launch_fused2(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int fused2_max_cols(int dtype);
 int launch_fused3(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
+int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
+int fused4_max_cols(int dtype);
 int fused3_max_cols(int dtype);
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)
