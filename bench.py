@@ -327,7 +327,7 @@ def run_ours(args):
                        "K_in": args.inner, "placement": "node-major" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (A = %.1f GB/rank)" % (A_bytes / 1e9),
                        "sweeps_per_s": sweeps / (ms / 1e3), "setup_wall_s": setup_wall,
-                       "inner_sweep": "fused single HBM pass (k_fused2: one CTA per SM, SURVEY 8(f)1)" if fused_mode
+                       "inner_sweep": "fused single HBM pass (k_fused4: CTA-pair clusters, SURVEY 8(f)1)" if fused_mode
                        else "two-pass (GEMV-T + GEMV)",
                        "two_pass_equivalent_GBps": (2 * A_bytes + nl * n * n * s) * sweeps / (ms / 1e3) / 1e9},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

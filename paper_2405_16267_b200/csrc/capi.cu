@@ -80,8 +80,11 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     int node, block, user_index, li, jl;
     const void* A;
     int64_t lda, m, c0, nj;
-    void* H;
-    int64_t ldh;
+    void* H;         // tall block: H = (rho_l A^T A + c I)^{-1} (nj x nj); fat block (Woodbury,
+    int64_t ldh;     // m < nj): K^{-1} = ((c/rho_l) I + A A^T)^{-1} (m x m)
+    bool fat = false;
+    int64_t kd = 0;  // factor order: fat ? m : nj
+    double* t1 = nullptr;   // fat: A r (m * C)
     double *x, *u, *r, *p, *partial, *pobj;
     double* fpart;   // fused sweep: [node chunks][nj] partial products of A^T q
     double* partial2 = nullptr;   // fused v2: [CTAs touching the node][nj]
@@ -122,6 +125,7 @@ struct bicadmm_handle {
     bicadmm_params prm{};
     bicadmm_comm* comm = nullptr;
     bool split_blocks = false;  // some node's blocks live on other ranks
+    bool any_fat = false;       // some local block takes the Woodbury path
     cudaStream_t st = nullptr;
     int sm_count = 148, gemv_cap = 148;
     size_t ws_bytes = 0;
@@ -297,13 +301,21 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         L.jl = h->nod.back().np++;
     }
     const int nl = (int)h->nod.size();
-    int64_t njmax = 0;
-    for (auto& L : h->blk) njmax = std::max(njmax, L.nj);
+    // Woodbury fat-block path (R27) unless BICADMM_WOODBURY=0
+    const char* wb = getenv("BICADMM_WOODBURY");
+    const bool wb_on = !(wb && atoi(wb) == 0);
+    int64_t kdmax = 0;
+    for (auto& L : h->blk) {
+        L.fat = wb_on && L.m < L.nj;
+        L.kd = L.fat ? L.m : L.nj;
+        kdmax = std::max(kdmax, L.kd);
+        h->any_fat = h->any_fat || L.fat;
+    }
     // matrices
     const size_t es = P->dtype == BICADMM_F64 ? 8 : 4;
     for (auto& L : h->blk) {
-        L.ldh = rup(L.nj, 4);
-        L.H = b.take(es * (size_t)(L.ldh * L.nj));
+        L.ldh = rup(L.kd, 4);
+        L.H = b.take(es * (size_t)(L.ldh * L.kd));
     }
     // global vectors
     h->x_all = b.arr<double>(lenp * nl);
@@ -356,9 +368,10 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         L.xt = C > 1 ? b.arr<double>(L.nj * C) : nullptr;
         L.pobj = nd.pobj_base + (base ? (int64_t)L.jl * nd.m * C : 0);
         L.partial = b.arr<double>(need[k]);
+        L.t1 = L.fat ? b.arr<double>(L.m * C) : nullptr;
     }
     // setup scratch: FP64 Gram / factor workspace
-    const int64_t ldg = rup(njmax, 8);
+    const int64_t ldg = rup(kdmax, 8);
     h->mask = b.arr<double>(len);
     h->cg_r = b.arr<double>(len);
     h->cg_p = b.arr<double>(len);
@@ -420,8 +433,8 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         for (auto& L : h->blk)
             if (L.jl == 0) L.partial2 = b.arr<double>(std::max<int64_t>(1, h->f2_cta_n[L.li]) * L.nj * C);
     }
-    h->gram = b.arr<double>(ldg * njmax);
-    h->fws = b.arr<double>((int64_t)factor_ws_doubles(njmax));
+    h->gram = b.arr<double>(ldg * kdmax);
+    h->fws = b.arr<double>((int64_t)factor_ws_doubles(kdmax));
     return b.off + 256;
 }
 
@@ -511,7 +524,7 @@ static bool fused2_eligible(bicadmm_handle* h, int kind = 2) {
     for (auto& nd : h->nod) if (nd.np != 1) return false;
     const int64_t cap = kind == 4 ? fused4_max_cols(h->dtype) : kind == 3 ? fused3_max_cols(h->dtype)
                                                                             : fused2_max_cols(h->dtype);
-    for (auto& L : h->blk) if (L.nj > cap || (kind == 4 && L.nj % 8)) return false;
+    for (auto& L : h->blk) if (L.fat || L.nj > cap || (kind == 4 && L.nj % 8)) return false;
     if (kind == 4 && h->sm_count < 2) return false;
     return true;
 }
@@ -712,6 +725,7 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     build_descs(h);
     {   // inner-sweep schedule (bicadmm_params.sweep)
         bool ok1 = !h->split_blocks && h->C == 1 && (int)h->nod.size() <= kMaxDesc;
+        for (auto& L : h->blk) ok1 = ok1 && !L.fat;
         for (auto& nd : h->nod) ok1 = ok1 && nd.np <= kFMaxBlk;
         const bool ok2 = fused2_eligible(h);
         const bool ok3 = fused2_eligible(h, 3);
@@ -722,9 +736,10 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             if (!ok1 && !ok2 && !ok3 && !ok4) { delete h; return BICADMM_ERR_INVALID; }
             kind = ok4 ? 4 : ok3 ? 3 : ok2 ? 2 : 1;
         } else if (R->sweep == 0) {
-            // auto = two-pass: measured on B200 (profiles/r01_summary.md) both fused kernels are
-            // slower than the two HBM-roofline passes (per-row serial prox / L2 re-read waits)
-            kind = 0;
+            // auto: the CTA-pair single-pass sweep (k_fused4) where eligible -- measured on B200
+            // (profiles/r01_summary.md) 1.45 ms vs 2.43 ms for the two HBM passes on configs[1];
+            // kinds 1-3 are slower than the two-pass sweep, which is taken otherwise
+            kind = ok4 ? 4 : 0;
         }
         if (fk && kind != 0) {
             const int want = atoi(fk);
@@ -771,9 +786,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     cudaEventRecord(h->e0, h->st);
     const double c = R->lambda / (double)P->N + R->rho_c;   // 1/(N gamma) + rho_c
     for (auto& L : h->blk) {
-        const int64_t ldg = rup(L.nj, 8);
-        rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, h->gram, ldg, false, h->st);
-        if (!rc) rc = factor_inverse(L.nj, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
+        const int64_t ldg = rup(L.kd, 8);
+        if (L.fat)   // K = (c/rho_l) I + A A^T  (Woodbury, R27)
+            rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, h->gram, ldg, h->st);
+        else         // F = rho_l A^T A + c I  (Eq. (24))
+            rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, h->gram, ldg, false, h->st);
+        if (!rc) rc = factor_inverse(L.kd, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
         if (rc) {
             std::string msg = rc == BICADMM_ERR_CUDA ? std::string("factor: ") + cudaGetErrorString(cudaGetLastError())
                                                      : std::string("factor: matrix not positive definite");
@@ -863,6 +881,14 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
         const LBlock& L = h->blk[k];
         if (!act[L.li]) continue;
         gt.push_back(h->gt[k]);
+        if (L.fat) {   // t1 = A r ; p = (1/rho_l) K^{-1} t1   (x deferred: materialize_x)
+            GemvDesc d1{L.A, L.lda, L.m, L.nj, L.r, L.t1, 0, L.xt};
+            hx.push_back(d1);
+            GemvDesc d2{L.H, L.ldh, L.m, L.m, L.t1, L.p, 0, L.xt};
+            d2.alpha = 1.0 / h->prm.rho_l;
+            ax.push_back(d2);
+            continue;
+        }
         GemvDesc d1{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0, L.xt};
         hx.push_back(d1);
         GemvDesc d2{L.A, L.lda, L.m, L.nj, L.x, L.p, 0, L.xt};
@@ -911,6 +937,34 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
         h->pending.push_back({3, ev[3], ev[4], lc[4] - lc[3]});
         h->pending.push_back({4, ev[4], ev[5], lc[5] - lc[4]});
         h->pending.push_back({5, ev[5], ev[6], lc[6] - lc[5]});
+    }
+    return BICADMM_OK;
+}
+
+// Fat blocks (Woodbury, R27) carry p_ij = A_ij x_ij exactly through the sweep
+// without forming x_ij; x_ij = (r - rho_l A^T p_ij) / c is materialized only where it is
+// read: before the outer step (Collect, Eq. (7)) and per sweep in tolerance mode.
+static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
+    std::vector<char> act(h->nod.size(), 0);
+    for (int li : nodes) act[li] = 1;
+    std::vector<GemvTDesc> gt;
+    for (size_t k = 0; k < h->blk.size(); ++k) {
+        const LBlock& L = h->blk[k];
+        if (!L.fat || !act[L.li]) continue;
+        GemvTDesc g = h->gt[k];
+        g.delta = nullptr; g.z = L.r; g.u = nullptr; g.r = L.x;
+        gt.push_back(g);
+    }
+    if (gt.empty()) return BICADMM_OK;
+    cudaEvent_t a = nullptr, b = nullptr;
+    const int64_t l0 = g_launches.load();
+    if (h->prof) { a = next_event(h); cudaEventRecord(a, h->st); }
+    const double c = h->prm.lambda / (double)h->N + h->prm.rho_c;
+    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), -h->prm.rho_l / c, 1.0 / c, h->st, nullptr, h->C));
+    if (h->prof) {
+        b = next_event(h);
+        cudaEventRecord(b, h->st);
+        h->pending.push_back({0, a, b, g_launches.load() - l0});
     }
     return BICADMM_OK;
 }
@@ -1020,6 +1074,12 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
                 int rc = inner_sweep(h, active);
                 if (rc) return rc;
             }
+            std::vector<int> swept;
+            for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > 0) swept.push_back((int)li);
+            if (h->any_fat) {
+                int rc = materialize_x(h, swept);
+                if (rc) return rc;
+            }
         } else {
             // tolerance mode: sweep node i until ||abar - obar|| <= eps sqrt(m_i C) and
             // ||x_i^new - x_i^old|| <= eps, at most max_inner sweeps
@@ -1028,6 +1088,7 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
             std::vector<double> res, dx;
             for (int sw = 0; sw < h->prm.max_inner && !active.empty(); ++sw) {
                 int rc = inner_sweep(h, active, true);
+                if (!rc && h->any_fat) rc = materialize_x(h, active);
                 if (!rc) rc = inner_criteria(h, active, res, dx);
                 if (rc) return rc;
                 std::vector<int> still;

@@ -158,6 +158,18 @@ int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, do
     return gemm<float, double, false, false>(g, s);
 }
 
+int launch_gram_rows(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag,
+                     double* G, int64_t ldg, cudaStream_t s) {
+    GemmArgs g{};
+    g.M = m; g.N = m; g.K = nj;
+    g.alpha = alpha; g.beta = 0.0; g.diag = diag;
+    g.A = A; g.lda = lda; g.B = A; g.ldb = lda; g.C = G; g.ldc = ldg;
+    g.lower_only = 1; g.mirror = 0; g.tri_k = 0;
+    // A A^T: A(i,k) = A[i*lda + k] (stored M x K), B(k,j) = A[j*lda + k] (stored N x K)
+    if (dtype == BICADMM_F64) return gemm<double, double, true, true>(g, s);
+    return gemm<float, double, true, true>(g, s);
+}
+
 // ------------------------------------------------------------------ Cholesky diag block
 // One CTA factors the kn x kn diagonal block (kn <= 64) of F in place (lower, upper
 // zeroed) and writes W_kk = L_kk^{-1} (lower) into Wd.  Unblocked right-looking

@@ -20,6 +20,7 @@
 // HBM exactly once per sweep; partial products are written per cluster and reduced
 // in fixed order by the next sweep's Eq. (24) epilogue (bit-reproducible).
 #include <cfloat>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -30,9 +31,10 @@ constexpr int kF4Main = 12;                    // main warps per CTA
 constexpr int kF4Prox = 3;                     // prox warps per CTA
 constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp = 512
 constexpr int kF4MainT = 32 * kF4Main;         // 384
-constexpr int kF4Ring = 4;                     // half-row ring
-constexpr int kF4D = 2;                        // axpy delay (rows)
-constexpr int kF4Q = 8;                        // dot / q slots (>= lag window, see below)
+constexpr int kF4RingMax = 8;                  // half-row ring depth (runtime nring <= 8, by smem)
+constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
+constexpr int kF4DL2 = 8;                      // axpy delay when the axpy re-reads the row from L2
+constexpr int kF4Q = 32;                       // dot / q slots (>= delay + lag window)
 
 __device__ __forceinline__ double f4_sigmoid(double a) {
     if (a >= 0.0) return 1.0 / (1.0 + exp(-a));
@@ -116,6 +118,13 @@ __device__ __forceinline__ void mb4_wait_cluster(uint64_t* b, unsigned parity) {
     for (long long it = 0; !mb4_try_cluster(b, parity); ++it)
         if (it > (1ll << 26)) asm volatile("trap;");
 }
+// asynchronous remote store that completes 8 bytes of the peer's mbarrier transaction
+// count: no cluster-scope release fence (MEMBAR.GPU) per row, unlike st + remote arrive
+__device__ __forceinline__ void st_async_f64(unsigned cluster_addr, double v, unsigned cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "d"(v), "r"(cluster_bar)
+                 : "memory");
+}
 __device__ __forceinline__ void st_cluster_f64(unsigned cluster_addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cluster_addr), "d"(v) : "memory");
 }
@@ -129,22 +138,35 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <typename T, int E>
+// MODE 0: the axpy of row k - 2 reads the smem ring (slot held until then);
+// MODE 1: the axpy re-reads half-row k - kF4DL2 from L2 (slot released after the dot);
+// MODE 2: each thread keeps its own columns of rows k-1, k-2 in registers (a delay
+//         line), x lives in smem, and the slot is released right after the dot -> the
+//         ring keeps nring - 1 half-rows in flight.
+template <typename T, int E, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
-    k_fused4(const Fused2Args a, int loss, double rho) {
+    k_fused4(const Fused2Args a, int loss, double rho, int nring) {
+    constexpr bool L2AX = MODE == 1;
+    constexpr int D = L2AX ? kF4DL2 : kF4D;
     extern __shared__ __align__(128) unsigned char f4_smem[];
-    T* ring = reinterpret_cast<T*>(f4_smem);             // kF4Ring x half_pad elements
+    T* ring = reinterpret_cast<T*>(f4_smem);             // nring x half_pad elements
     __shared__ double dotp[kF4Q][2 * kF4Main];            // [slot][cta * 12 + warp]
     __shared__ double qv[kF4Q];
-    __shared__ __align__(8) uint64_t bar_full[kF4Ring], bar_empty[kF4Ring], bar_dot[kF4Q], bar_q[kF4Q];
+    __shared__ __align__(8) uint64_t bar_full[kF4RingMax], bar_empty[kF4RingMax], bar_dot[kF4Q], bar_q[kF4Q];
     const unsigned h = cluster_rank();                     // column half owned by this CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t clu = blockIdx.x >> 1, nclu = gridDim.x >> 1;
     const int64_t rb = clu * a.total_rows / nclu, re = (clu + 1) * a.total_rows / nclu;
     const int64_t half_pad = ((a.max_cols_pad / 2 + 3) / 4) * 4 + 4;   // elements per ring slot (>= ch)
+    // ring position (slot, phase of its w-th use) advanced incrementally: no division by nring
+    struct RingPos {
+        int s = 0;
+        unsigned ph = 0;
+        __device__ void next(int n) { if (++s == n) { s = 0; ph ^= 1u; } }
+    };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kF4Ring; ++s) { mb4_init(&bar_full[s], 1); mb4_init(&bar_empty[s], kF4Main); }
-        for (int s = 0; s < kF4Q; ++s) { mb4_init(&bar_dot[s], 2 * kF4Main); mb4_init(&bar_q[s], 1); }
+        for (int s = 0; s < nring; ++s) { mb4_init(&bar_full[s], 1); mb4_init(&bar_empty[s], kF4Main); }
+        for (int s = 0; s < kF4Q; ++s) { mb4_init(&bar_dot[s], kF4Main); mb4_init(&bar_q[s], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync_all();   // barriers of both CTAs initialised before any remote arrive
@@ -168,11 +190,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         // ------------------------------------------------------------ producer (lane 0)
         if (lane == 0) {
             int nd = nd0;
-            for (int64_t r = rb; r < re; ++r) {
+            RingPos pw;
+            for (int64_t r = rb; r < re; ++r, pw.next(nring)) {
                 nd = node_of(r, nd);
-                const int s = (int)((r - rb) % kF4Ring);
-                const int64_t u = (r - rb) / kF4Ring;
-                if (u >= 1) mb4_wait_cta(&bar_empty[s], (unsigned)((u - 1) & 1));
+                const int s = pw.s;
+                if (r - rb >= nring) mb4_wait_cta(&bar_empty[s], pw.ph ^ 1u);   // (w-1)-th release
                 int64_t c0, cn;
                 half_range(nd, c0, cn);
                 const unsigned bytes = (unsigned)(cn * (int64_t)sizeof(T));
@@ -183,7 +205,90 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                                  &bar_full[s]);
             }
         }
-    } else if (warp < kF4Main) {
+    } else if (MODE == 2 && warp < kF4Main) {
+        // ------------------------------------------------------------ main warps, register delay line
+        const int mt = threadIdx.x;
+        const unsigned peer = h ^ 1u;
+        double* xs = reinterpret_cast<double*>(f4_smem + (size_t)nring * half_pad * sizeof(T));
+        int ndd = nd0, nda = nd0;
+        double acc[E], h0[E], h1[E];
+        int64_t hc0, hcn, ac0, acn;
+        auto load_x = [&](int nd) {   // main warps only (named barrier 1)
+            half_range(nd, hc0, hcn);
+            asm volatile("bar.sync 1, %0;" ::"n"(kF4MainT));
+            for (int64_t c = mt; c < hcn; c += kF4MainT) xs[c] = a.x[nd][hc0 + c];
+            asm volatile("bar.sync 1, %0;" ::"n"(kF4MainT));
+        };
+        load_x(ndd);
+        half_range(nda, ac0, acn);
+#pragma unroll
+        for (int e = 0; e < E; ++e) { acc[e] = 0.0; h0[e] = 0.0; h1[e] = 0.0; }
+        auto flush = [&](int node) {
+            double* out = a.partial[node] + (clu - a.cta_lo[node]) * a.ncols[node] + ac0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t c = mt + (int64_t)kF4MainT * e;
+                if (c < acn) out[c] = acc[e];
+                acc[e] = 0.0;
+            }
+        };
+        RingPos pd;
+        auto step = [&](int64_t k, double (&H)[E]) {
+            double tmp[E];
+            if (k < re) {
+                const int nn2 = node_of(k, ndd);
+                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
+                const int s = pd.s;
+                mb4_wait_cta(&bar_full[s], pd.ph);
+                pd.next(nring);
+                const T* row = ring + s * half_pad;
+                double dot = 0.0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int64_t c = mt + (int64_t)kF4MainT * e;
+                    tmp[e] = c < hcn ? (double)row[c] : 0.0;
+                    if (c < hcn) dot = fma(tmp[e], xs[c], dot);
+                }
+                __syncwarp();
+                if (lane == 0) mb4_arrive_local(&bar_empty[s]);   // slot free: row k now in registers
+                if (!a.active[ndd]) dot = 0.0;
+                dot = warp_sum(dot);
+                if (lane == 0) {
+                    const int q = (int)((k - rb) % kF4Q);
+                    const int idx = (int)h * kF4Main + warp;
+                    dotp[q][idx] = dot;
+                    st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
+                    if (warp == 0) mb4_expect_tx(&bar_dot[q], 8u * kF4Main);   // the peer's 12 stores
+                    else mb4_arrive_local(&bar_dot[q]);
+                }
+            }
+            const int64_t ra = k - 2;   // its columns are in H
+            if (ra >= rb && ra < re) {
+                const int nn2 = node_of(ra, nda);
+                if (nn2 != nda) {
+                    if (a.active[nda]) flush(nda);
+                    nda = nn2;
+                    half_range(nda, ac0, acn);
+                }
+                const int q = (int)((ra - rb) % kF4Q);
+                mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
+                const double qq = qv[q];
+                if (a.active[nda]) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = fma(H[e], qq, acc[e]);
+                }
+            }
+            if (k < re) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) H[e] = tmp[e];
+            }
+        };
+        for (int64_t k = rb; k < re + 2; k += 2) {
+            step(k, h0);
+            step(k + 1, h1);
+        }
+        if (a.active[nda]) flush(nda);
+    } else if (MODE != 2 && warp < kF4Main) {
         // ------------------------------------------------------------ main warps
         const int mt = threadIdx.x;
         const unsigned peer = h ^ 1u;
@@ -212,12 +317,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                 acc[e] = 0.0;
             }
         };
-        for (int64_t k = rb; k < re + kF4D; ++k) {
+        RingPos pd, pa;
+        for (int64_t k = rb; k < re + D; ++k) {
             if (k < re) {
                 const int nn2 = node_of(k, ndd);
                 if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
-                const int s = (int)((k - rb) % kF4Ring);
-                mb4_wait_cta(&bar_full[s], (unsigned)(((k - rb) / kF4Ring) & 1));
+                const int s = pd.s;
+                mb4_wait_cta(&bar_full[s], pd.ph);
+                pd.next(nring);
                 const T* row = ring + s * half_pad;
                 double dot = 0.0;
                 if (a.active[ndd]) {
@@ -227,17 +334,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                         if (c < hcn) dot = fma((double)row[c], xr[e], dot);
                     }
                 }
+                if constexpr (L2AX) {   // ring slot free as soon as every warp has read it
+                    __syncwarp();
+                    if (lane == 0) mb4_arrive_local(&bar_empty[s]);
+                }
                 dot = warp_sum(dot);
                 if (lane == 0) {
                     const int q = (int)((k - rb) % kF4Q);
                     const int idx = (int)h * kF4Main + warp;
                     dotp[q][idx] = dot;
-                    st_cluster_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot);
-                    mb4_arrive_local(&bar_dot[q]);
-                    mb4_arrive_remote(mapa(smem_u32(&bar_dot[q]), peer));
+                    st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
+                    if (warp == 0) mb4_expect_tx(&bar_dot[q], 8u * kF4Main);   // the peer's 12 stores
+                    else mb4_arrive_local(&bar_dot[q]);
                 }
             }
-            const int64_t ra = k - kF4D;
+            const int64_t ra = k - D;
             if (ra >= rb) {
                 const int nn2 = node_of(ra, nda);
                 if (nn2 != nda) {
@@ -246,19 +357,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                     half_range(nda, ac0, acn);
                 }
                 const int q = (int)((ra - rb) % kF4Q);
-                mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
-                const double qq = qv[q];
-                const int s = (int)((ra - rb) % kF4Ring);
-                const T* row = ring + s * half_pad;
-                if (a.active[nda]) {
+                const bool on = a.active[nda];
+                if constexpr (L2AX) {
+                    // issue the L2 re-read of half-row ra before waiting for its q
+                    const T* grow = static_cast<const T*>(a.A[nda]) + (ra - a.row_off[nda]) * a.lda[nda] + ac0;
+                    double v[E];
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
                         const int64_t c = mt + (int64_t)kF4MainT * e;
-                        if (c < acn) acc[e] = fma((double)row[c], qq, acc[e]);
+                        v[e] = (on && c < acn) ? (double)__ldg(grow + c) : 0.0;
                     }
+                    mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
+                    const double qq = qv[q];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[e] = fma(v[e], qq, acc[e]);
+                } else {
+                    mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
+                    const double qq = qv[q];
+                    const int s = pa.s;
+                    pa.next(nring);
+                    const T* row = ring + s * half_pad;
+                    if (on) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const int64_t c = mt + (int64_t)kF4MainT * e;
+                            if (c < acn) acc[e] = fma((double)row[c], qq, acc[e]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mb4_arrive_local(&bar_empty[s]);
                 }
-                __syncwarp();
-                if (lane == 0) mb4_arrive_local(&bar_empty[s]);
             }
         }
         if (a.active[nda]) flush(nda);
@@ -303,23 +431,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
 
 int fused4_max_cols(int dtype) { return dtype == BICADMM_F64 ? 2 * kF4MainT * 16 : 2 * kF4MainT * 16; }
 
-template <typename T>
+static size_t f4_slot_bytes(const Fused2Args& a, size_t es) { return (size_t)(((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * es; }
+static int f4_mode() {
+    static int m = [] { const char* e = getenv("BICADMM_F4_MODE"); int v = e ? atoi(e) : 0; return v >= 0 && v <= 2 ? v : 0; }();
+    return m;
+}
+static size_t f4_xs_bytes(const Fused2Args& a) { return f4_mode() == 2 ? f4_slot_bytes(a, 8) : 0; }
+static int f4_ring(const Fused2Args& a, size_t es) {
+    const char* e = getenv("BICADMM_F4_RING");
+    int r = (int)((210 * 1024 - f4_xs_bytes(a)) / f4_slot_bytes(a, es));
+    if (e) r = atoi(e) < r ? atoi(e) : r;
+    return r > kF4RingMax ? kF4RingMax : r;
+}
+
+template <typename T, int MODE>
 static int f4_launch(int E, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
-    const size_t smem = (size_t)kF4Ring * (((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * sizeof(T);
+    const int nring = f4_ring(a, sizeof(T));
+    if (nring < 4) return BICADMM_ERR_INVALID;
+    const size_t smem = (size_t)nring * f4_slot_bytes(a, sizeof(T)) + f4_xs_bytes(a);
 #define F4_CASE(EE)                                                                                            \
     case EE: {                                                                                                 \
         static bool set = false;                                                                               \
         if (!set) {                                                                                            \
-            if (cudaFuncSetAttribute(k_fused4<T, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != \
-                cudaSuccess)                                                                                   \
+            if (cudaFuncSetAttribute(k_fused4<T, EE, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                     212 * 1024) != cudaSuccess)                                               \
                 return BICADMM_ERR_CUDA;                                                                       \
             set = true;                                                                                        \
         }                                                                                                      \
-        k_fused4<T, EE><<<grid, kF4Threads, smem, s>>>(a, loss, rho);                                          \
+        k_fused4<T, EE, MODE><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring);                             \
         break;                                                                                                 \
     }
     switch (E) {
-        F4_CASE(2) F4_CASE(4) F4_CASE(8) F4_CASE(12) F4_CASE(16)
+        F4_CASE(2) F4_CASE(4) F4_CASE(8) F4_CASE(12) F4_CASE(14) F4_CASE(16)
     default: return BICADMM_ERR_INVALID;
     }
 #undef F4_CASE
@@ -331,11 +474,18 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     for (int k = 0; k < a.nn; ++k) maxc = a.ncols[k] > maxc ? a.ncols[k] : maxc;
     const int64_t half = (maxc + 1) / 2 + 2;
     const int64_t e = (half + kF4MainT - 1) / kF4MainT;
-    const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 16 ? 16 : -1;
-    const size_t smem = (size_t)kF4Ring * (((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * (dtype == BICADMM_F64 ? 8 : 4);
-    if (E < 0 || smem > 200 * 1024 || (grid & 1)) return BICADMM_ERR_INVALID;
+    const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 14 ? 14 : e <= 16 ? 16 : -1;
+    if (E < 0 || f4_ring(a, dtype == BICADMM_F64 ? 8 : 4) < 4 || (grid & 1)) return BICADMM_ERR_INVALID;
     for (int k = 0; k < a.nn; ++k) if (a.ncols[k] % 8) return BICADMM_ERR_INVALID;
-    int rc = dtype == BICADMM_F64 ? f4_launch<double>(E, a, loss, rho, grid, s) : f4_launch<float>(E, a, loss, rho, grid, s);
+    // BICADMM_F4_MODE: 0 (default) ring-held rows, 1 L2 re-read, 2 register delay line
+    const int mode = f4_mode();
+    int rc;
+    if (dtype == BICADMM_F64)
+        rc = mode == 2 ? f4_launch<double, 2>(E, a, loss, rho, grid, s)
+           : mode == 1 ? f4_launch<double, 1>(E, a, loss, rho, grid, s) : f4_launch<double, 0>(E, a, loss, rho, grid, s);
+    else
+        rc = mode == 2 ? f4_launch<float, 2>(E, a, loss, rho, grid, s)
+           : mode == 1 ? f4_launch<float, 1>(E, a, loss, rho, grid, s) : f4_launch<float, 0>(E, a, loss, rho, grid, s);
     if (rc) return rc;
     BIC_LAUNCHED();
     return BICADMM_OK;

@@ -74,7 +74,7 @@ __device__ __forceinline__ void gemv_rows_f64(const GemvDesc& D, int64_t r0, int
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
         const double s = warp_sum(acc[rr]);
-        if (lane == rr && r0 + rr < D.rows) D.y[r0 + rr] = s;
+        if (lane == rr && r0 + rr < D.rows) D.y[r0 + rr] = D.alpha * s;
     }
 }
 
@@ -131,7 +131,7 @@ __device__ __forceinline__ void gemv_rows_f32(const GemvDesc& D, int64_t r0, int
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
         const double s = warp_sum(acc[rr]);
-        if (lane == rr && r0 + rr < D.rows) D.y[r0 + rr] = s;
+        if (lane == rr && r0 + rr < D.rows) D.y[r0 + rr] = D.alpha * s;
     }
 }
 

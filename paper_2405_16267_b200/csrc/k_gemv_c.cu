@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kGemvCThreads) k_gemv_c(const __grid_constant_
             for (int c = 0; c < CM; ++c) {
                 if (c < C) {
                     const double sum = warp_sum(acc[rr][c]);
-                    if (lane == 0 && r0 + rr < D.rows) D.y[(r0 + rr) * C + c] = sum;
+                    if (lane == 0 && r0 + rr < D.rows) D.y[(r0 + rr) * C + c] = D.alpha * sum;
                 }
             }
     }

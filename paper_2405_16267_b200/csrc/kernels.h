@@ -15,6 +15,7 @@ struct GemvDesc {
     double* y;
     int64_t task_begin;  // filled by the launcher
     double* xt = nullptr;   // C > 1: scratch (cols * C) for the class-major copy of x
+    double alpha = 1.0;     // y = alpha * (A x)
 };
 int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s, int C = 1);
 int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
@@ -67,6 +68,10 @@ int launch_loss(int loss, int dtype, int C, ProxNode* nodes, int nn, cudaStream_
 // F = alpha A^T A + diag I (lower triangle or full) into FP64 G (ldg).
 int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
                 double diag, double* G, int64_t ldg, bool full, cudaStream_t s);
+// K = alpha A A^T + diag I (m x m, lower triangle or full) into FP64 G (ldg): the Woodbury
+// kernel matrix of fat blocks (m_i < n_j).
+int launch_gram_rows(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
+                     double diag, double* G, int64_t ldg, cudaStream_t s);
 // In-place: G (nj x nj FP64, lower triangle holding F) -> H = F^{-1} written to H (dtype, ldh).
 // ws: FP64 scratch of factor_ws_doubles(nj) doubles.
 size_t factor_ws_doubles(int64_t nj);

@@ -68,6 +68,10 @@ def test_fp64_iterates_match_oracle(bc, orc, case, sweep):
     if C > 1 and sweep == 2:
         pytest.skip("fused single-pass sweep is C == 1 only (softmax runs two-pass)")
     solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, sweep=sweep)
+    _check_fp64(solver, rep, zs, xs, ref, K)
+
+
+def _check_fp64(solver, rep, zs, xs, ref, K):
     tr_g = solver.trace()
     tr_o = ref["trace"]
     assert tr_g.shape == tr_o.shape
@@ -211,3 +215,68 @@ def test_fused_kinds_single_block(bc, orc, kind):
             assert solver.support().tolist() == ref["support"].tolist()
     finally:
         del os.environ["BICADMM_FUSED_KIND"]
+
+
+# Woodbury fat-block path (DESIGN R27): blocks with m_i < n_j factor the m_i x m_i
+# matrix K = (c/rho_l) I + A A^T instead of the n_j x n_j F; x_ij is materialized only
+# where read.  Same oracle (which always solves the n_j x n_j system), same 1e-9 bar.
+FAT_CASES = [
+    # name, N, m_i, n, kappa, loss, M, K_outer, K_in[, C]
+    ("ls_fat", 2, 80, 300, 8, "ls", 1, 15, 5),
+    ("logistic_fat_blocks2", 3, 90, 400, 10, "logistic", 2, 12, 5),
+    ("hinge_fat_blocks3", 2, 150, 600, 8, "hinge", 3, 10, 4),
+    ("softmax_fat_c3", 2, 60, 200, 6, "softmax", 1, 8, 4, 3),
+    ("logistic_mixed_fat_tall", 2, 200, 401, 8, "logistic", 2, 10, 4),
+    ("ls_fat_ragged_blocks4", 2, 77, 1030, 12, "ls", 4, 10, 3),
+]
+
+
+@pytest.mark.parametrize("case", FAT_CASES, ids=[c[0] for c in FAT_CASES])
+def test_woodbury_fat_blocks_match_oracle(bc, orc, case):
+    _, N, m, n, kappa, loss, M, K, K_in = case[:9]
+    C = case[9] if len(case) > 9 else 1
+    assert m < max(np.diff(dg.block_partition(n, M)))    # at least one block takes the fat path
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, sweep=1)
+    _check_fp64(solver, rep, zs, xs, ref, K)
+
+
+def test_woodbury_fp32_and_schedule(bc, orc):
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 90, 400, 10, "logistic", 2, 10, 5, dtype=torch.float32)
+    for k in range(10):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-4, k
+    assert solver.support().tolist() == ref["support"].tolist()
+    # schedule with zero-sweep nodes: x of an unswept node must stay as it was
+    P = dg.generate(3, 70, 240, 6, "logistic", seed=5)
+    cs = dg.block_partition(240, 2)
+    K = 5
+    sched = np.array([[1, 4, 2], [3, 0, 1], [0, 1, 1], [2, 2, 0], [4, 0, 3]], dtype=np.int32)
+    prm = dict(kappa=6, max_outer=K, inner_fixed=3, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(**prm), cs)
+    solver.set_schedule(sched)
+    solver.iterate(K)
+    ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs)),
+                  orc.Params(**prm), schedule=sched)
+    assert _rel(solver.z, ref["z"]) <= 1e-9
+
+
+def test_woodbury_tol_mode(bc, orc):
+    P = dg.generate(3, 100, 360, 6, "logistic", seed=22)
+    cs = dg.block_partition(360, 2)
+    K = 6
+    prm = dict(kappa=6, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=60, refit=0,
+               eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    solver = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(sweep=1, **prm), cs)
+    solver.iterate(K)
+    counts = solver.get(bc.FIELD_INNER_COUNTS, np.int32).reshape(K, 3)
+    pb = orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs))
+    own = orc.run(pb, orc.Params(**prm))
+    rep = orc.run(pb, orc.Params(**prm), schedule=counts)
+    assert _rel(solver.z, rep["z"]) <= 1e-9
+    assert np.mean(counts == own["inner_counts"]) >= 0.8
+
+
+def test_woodbury_fat_refuses_fused_sweep(bc):
+    P = dg.generate(2, 80, 300, 8, "ls", seed=1)
+    with pytest.raises(Exception):
+        bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls", bc.Params(kappa=8, sweep=2),
+                   dg.block_partition(300, 1))
