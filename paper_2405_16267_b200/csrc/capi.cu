@@ -85,6 +85,8 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     bool fat = false;
     int64_t kd = 0;  // factor order: fat ? m : nj
     double* t1 = nullptr;   // fat: A r (m * C)
+    bool hpack = false;     // H stored as packed lower tiles (k_symv.cu); C == 1 only
+    double* hpart = nullptr;
     double *x, *u, *r, *p, *partial, *pobj;
     double* fpart;   // fused sweep: [node chunks][nj] partial products of A^T q
     double* partial2 = nullptr;   // fused v2: [CTAs touching the node][nj]
@@ -313,9 +315,13 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     }
     // matrices
     const size_t es = P->dtype == BICADMM_F64 ? 8 : 4;
+    const char* hp = getenv("BICADMM_HPACK");
+    const bool hp_on = C == 1 && !(hp && atoi(hp) == 0);
     for (auto& L : h->blk) {
         L.ldh = rup(L.kd, 4);
-        L.H = b.take(es * (size_t)(L.ldh * L.kd));
+        L.hpack = hp_on;
+        L.H = b.take(es * (size_t)(L.hpack ? symv_packed_elems(L.kd) : L.ldh * L.kd));
+        L.hpart = L.hpack ? b.arr<double>(symv_part_doubles(L.kd)) : nullptr;
     }
     // global vectors
     h->x_all = b.arr<double>(lenp * nl);
@@ -791,7 +797,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, h->gram, ldg, h->st);
         else         // F = rho_l A^T A + c I  (Eq. (24))
             rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, h->gram, ldg, false, h->st);
-        if (!rc) rc = factor_inverse(L.kd, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
+        if (!rc && L.hpack) {   // full FP64 inverse into the (consumed) Gram scratch, then pack
+            rc = factor_inverse(L.kd, h->gram, ldg, h->gram, ldg, BICADMM_F64, h->fws, h->st);
+            if (!rc) rc = launch_symv_pack(P->dtype, L.kd, h->gram, ldg, L.H, h->st);
+        } else if (!rc) {
+            rc = factor_inverse(L.kd, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
+        }
         if (rc) {
             std::string msg = rc == BICADMM_ERR_CUDA ? std::string("factor: ") + cudaGetErrorString(cudaGetLastError())
                                                      : std::string("factor: matrix not positive definite");
@@ -811,16 +822,41 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
 }
 
 // ======================================================================= iterate
+// A batch of GEMV descriptors plus packed-symmetric H-applies (k_symv.cu), one phase.
+struct GemvList {
+    std::vector<GemvDesc> g;
+    std::vector<SymvDesc> s;
+    void gemv(const GemvDesc& d) { g.push_back(d); }
+    void happly(const LBlock& L, const double* x, double* y, double alpha) {   // y = alpha H x
+        if (L.hpack) {
+            SymvDesc d{};
+            d.H = L.H; d.n = L.kd; d.x = x; d.y = y; d.alpha = alpha; d.part = L.hpart;
+            s.push_back(d);
+        } else {
+            GemvDesc d{L.H, L.ldh, L.kd, L.kd, x, y, 0, L.xt};
+            d.alpha = alpha;
+            g.push_back(d);
+        }
+    }
+    int launch(bicadmm_handle* h) const;
+};
+
+int GemvList::launch(bicadmm_handle* h) const {
+    if (!g.empty()) H_RC(h, launch_gemv(h->dtype, const_cast<GemvDesc*>(g.data()), (int)g.size(), h->gemv_cap, h->st, h->C));
+    if (!s.empty()) H_RC(h, launch_symv_packed(h->dtype, s.data(), (int)s.size(), h->st));
+    return BICADMM_OK;
+}
+
 static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_nodes, bool tol) {
     std::vector<GemvTDesc> gt;
-    std::vector<GemvDesc> hx;
+    GemvList hx;
     std::vector<char> act(h->nod.size(), 0);
     for (int li : active_nodes) act[li] = 1;
     for (size_t k = 0; k < h->blk.size(); ++k) {
         const LBlock& L = h->blk[k];
         if (!act[L.li]) continue;
         gt.push_back(h->gtf[k]);
-        hx.push_back(GemvDesc{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0});
+        hx.happly(L, L.r, L.x, 1.0);
     }
     cudaEvent_t ev[4] = {};
     int64_t lc[4] = {};
@@ -836,7 +872,7 @@ static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_n
     if (tol)
         H_CUDA(h, cudaMemcpyAsync(h->x_old, h->x_all, sizeof(double) * h->lenp * h->nod.size(),
                                   cudaMemcpyDeviceToDevice, h->st));
-    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st, h->C));
+    H_RC(h, hx.launch(h));
     mark(2);
     for (size_t li = 0; li < h->nod.size() && h->fused_kind == 1; ++li)
         if (h->active_last[li] != (int)act[li]) {
@@ -873,7 +909,7 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     if (h->fused) return inner_sweep_fused(h, active_nodes, tol);
     // descriptors for the active nodes' blocks
     std::vector<GemvTDesc> gt;
-    std::vector<GemvDesc> hx, ax;
+    GemvList hx, ax;
     std::vector<ProxNode> px;
     std::vector<char> act(h->nod.size(), 0);
     for (int li : active_nodes) act[li] = 1;
@@ -882,17 +918,12 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
         if (!act[L.li]) continue;
         gt.push_back(h->gt[k]);
         if (L.fat) {   // t1 = A r ; p = (1/rho_l) K^{-1} t1   (x deferred: materialize_x)
-            GemvDesc d1{L.A, L.lda, L.m, L.nj, L.r, L.t1, 0, L.xt};
-            hx.push_back(d1);
-            GemvDesc d2{L.H, L.ldh, L.m, L.m, L.t1, L.p, 0, L.xt};
-            d2.alpha = 1.0 / h->prm.rho_l;
-            ax.push_back(d2);
+            hx.gemv(GemvDesc{L.A, L.lda, L.m, L.nj, L.r, L.t1, 0, L.xt});
+            ax.happly(L, L.t1, L.p, 1.0 / h->prm.rho_l);
             continue;
         }
-        GemvDesc d1{L.H, L.ldh, L.nj, L.nj, L.r, L.x, 0, L.xt};
-        hx.push_back(d1);
-        GemvDesc d2{L.A, L.lda, L.m, L.nj, L.x, L.p, 0, L.xt};
-        ax.push_back(d2);
+        hx.happly(L, L.r, L.x, 1.0);
+        ax.gemv(GemvDesc{L.A, L.lda, L.m, L.nj, L.x, L.p, 0, L.xt});
     }
     for (int li : active_nodes) {
         const LNode& nd = h->nod[li];
@@ -918,9 +949,9 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     if (tol)   // keep x^k for the ||x^{k+1} - x^k|| criterion
         H_CUDA(h, cudaMemcpyAsync(h->x_old, h->x_all, sizeof(double) * h->lenp * h->nod.size(),
                                   cudaMemcpyDeviceToDevice, h->st));
-    H_RC(h, launch_gemv(h->dtype, hx.data(), (int)hx.size(), h->gemv_cap, h->st, h->C));
+    H_RC(h, hx.launch(h));
     mark(3);
-    H_RC(h, launch_gemv(h->dtype, ax.data(), (int)ax.size(), h->gemv_cap, h->st, h->C));
+    H_RC(h, ax.launch(h));
     mark(4);
     if (h->split_blocks) {
         H_RC(h, launch_psum(h->C, px.data(), (int)px.size(), nullptr, h->st));

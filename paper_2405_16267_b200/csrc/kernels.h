@@ -18,6 +18,20 @@ struct GemvDesc {
     double alpha = 1.0;     // y = alpha * (A x)
 };
 int launch_gemv(int dtype, GemvDesc* d, int nd, int grid_cap, cudaStream_t s, int C = 1);
+
+// Packed symmetric H-apply (k_symv.cu): y = alpha * H x, H stored as lower 64x64 tiles.
+struct SymvDesc {
+    const void* H;      // symv_packed_elems(n) elements of the data dtype
+    int64_t n;
+    const double* x;
+    double* y;
+    double alpha = 1.0;
+    double* part;       // symv_part_doubles(n) scratch
+};
+int64_t symv_packed_elems(int64_t n);
+int64_t symv_part_doubles(int64_t n);
+int launch_symv_packed(int dtype, const SymvDesc* d, int nd, cudaStream_t s);
+int launch_symv_pack(int dtype, int64_t n, const double* G, int64_t ldg, void* Hp, cudaStream_t s);
 int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
 int gemv_grid_cap(int dtype, int sm_count);  // persistent grid size (resident CTAs)
 

@@ -280,3 +280,16 @@ def test_woodbury_fat_refuses_fused_sweep(bc):
     with pytest.raises(Exception):
         bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls", bc.Params(kappa=8, sweep=2),
                    dg.block_partition(300, 1))
+
+
+def test_full_h_layout_matches_oracle(bc, orc):
+    # BICADMM_HPACK=0: the unpacked n_j x n_j H (GEMV) instead of the packed lower tiles
+    import os
+    os.environ["BICADMM_HPACK"] = "0"
+    try:
+        for case in (CASES[3], FAT_CASES[1]):
+            _, N, m, n, kappa, loss, M, K, K_in = case[:9]
+            solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, sweep=1)
+            _check_fp64(solver, rep, zs, xs, ref, K)
+    finally:
+        del os.environ["BICADMM_HPACK"]
