@@ -84,7 +84,10 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     int64_t ldh;     // m < nj): K^{-1} = ((c/rho_l) I + A A^T)^{-1} (m x m)
     bool fat = false;
     int64_t kd = 0;  // factor order: fat ? m : nj
-    double* t1 = nullptr;   // fat: A r (m * C)
+    double* t1 = nullptr;   // fat: m * C scratch (A (z - u), then K^{-1} q)
+    double* w0 = nullptr;   // fat: (rho_c/rho_l) K^{-1} A (z - u), fixed within an inner loop
+    double* qd = nullptr;   // fat: q of the last sweep, then q - p (x materialization)
+    double* zu = nullptr;   // fat: z_j - u_ij (n_j * C)
     bool hpack = false;     // H stored as packed lower tiles (k_symv.cu); C == 1 only
     double* hpart = nullptr;
     double *x, *u, *r, *p, *partial, *pobj;
@@ -375,6 +378,9 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         L.pobj = nd.pobj_base + (base ? (int64_t)L.jl * nd.m * C : 0);
         L.partial = b.arr<double>(need[k]);
         L.t1 = L.fat ? b.arr<double>(L.m * C) : nullptr;
+        L.w0 = L.fat ? b.arr<double>(L.m * C) : nullptr;
+        L.qd = L.fat ? b.arr<double>(L.m * C) : nullptr;
+        L.zu = L.fat ? b.arr<double>(L.nj * C) : nullptr;
     }
     // setup scratch: FP64 Gram / factor workspace
     const int64_t ldg = rup(kdmax, 8);
@@ -910,18 +916,24 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     // descriptors for the active nodes' blocks
     std::vector<GemvTDesc> gt;
     GemvList hx, ax;
+    std::vector<FatEw> fq, fc;   // Woodbury blocks: q = p + delta; p = q + t1 + w0, qd = q - p
     std::vector<ProxNode> px;
     std::vector<char> act(h->nod.size(), 0);
     for (int li : active_nodes) act[li] = 1;
     for (size_t k = 0; k < h->blk.size(); ++k) {
         const LBlock& L = h->blk[k];
         if (!act[L.li]) continue;
-        gt.push_back(h->gt[k]);
-        if (L.fat) {   // t1 = A r ; p = (1/rho_l) K^{-1} t1   (x deferred: materialize_x)
-            hx.gemv(GemvDesc{L.A, L.lda, L.m, L.nj, L.r, L.t1, 0, L.xt});
-            ax.happly(L, L.t1, L.p, 1.0 / h->prm.rho_l);
+        if (L.fat) {
+            // Woodbury sweep entirely in m-space (R27):
+            //   p = (1/rho_l) K^{-1} A r = q - (c/rho_l) K^{-1} q + w0,  w0 = (rho_c/rho_l) K^{-1} A (z - u)
+            const double cc = h->prm.lambda / (double)h->N + h->prm.rho_c;
+            const int64_t mc = L.m * h->C;
+            fq.push_back(FatEw{L.p, h->nod[L.li].delta, nullptr, L.qd, nullptr, mc});
+            hx.happly(L, L.qd, L.t1, -cc / h->prm.rho_l);
+            fc.push_back(FatEw{L.qd, L.t1, L.w0, L.p, L.qd, mc});
             continue;
         }
+        gt.push_back(h->gt[k]);
         hx.happly(L, L.r, L.x, 1.0);
         ax.gemv(GemvDesc{L.A, L.lda, L.m, L.nj, L.x, L.p, 0, L.xt});
     }
@@ -943,15 +955,20 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     };
     mark(0);
     cudaEvent_t mid = h->prof ? next_event(h) : nullptr;
-    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid, h->C));
+    if (!gt.empty())
+        H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid, h->C));
+    else if (mid)
+        cudaEventRecord(mid, h->st);
     const int64_t l_partial = (int64_t)(gt.size() + kMaxDesc - 1) / kMaxDesc;
     mark(2);
     if (tol)   // keep x^k for the ||x^{k+1} - x^k|| criterion
         H_CUDA(h, cudaMemcpyAsync(h->x_old, h->x_all, sizeof(double) * h->lenp * h->nod.size(),
                                   cudaMemcpyDeviceToDevice, h->st));
+    if (!fq.empty()) H_RC(h, launch_fat_ew(fq.data(), (int)fq.size(), 0, h->st));
     H_RC(h, hx.launch(h));
     mark(3);
     H_RC(h, ax.launch(h));
+    if (!fc.empty()) H_RC(h, launch_fat_ew(fc.data(), (int)fc.size(), 1, h->st));
     mark(4);
     if (h->split_blocks) {
         H_RC(h, launch_psum(h->C, px.data(), (int)px.size(), nullptr, h->st));
@@ -973,8 +990,29 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
 }
 
 // Fat blocks (Woodbury, R27) carry p_ij = A_ij x_ij exactly through the sweep
-// without forming x_ij; x_ij = (r - rho_l A^T p_ij) / c is materialized only where it is
-// read: before the outer step (Collect, Eq. (7)) and per sweep in tolerance mode.
+// without forming x_ij; x_ij = (r - rho_l A^T p_ij) / c = (rho_l A^T (q - p) + rho_c (z - u)) / c
+// is materialized only where it is read: before the outer step (Collect, Eq. (7)) and per
+// sweep in tolerance mode.  fat_prepare computes the per-inner-loop constant
+// w0 = (rho_c/rho_l) K^{-1} A (z - u) (z and u are fixed during an inner loop).
+static int fat_prepare(bicadmm_handle* h, const std::vector<int>& nodes) {
+    std::vector<char> act(h->nod.size(), 0);
+    for (int li : nodes) act[li] = 1;
+    std::vector<FatEw> zu;
+    std::vector<GemvDesc> aw;
+    GemvList kw;
+    for (auto& L : h->blk) {
+        if (!L.fat || !act[L.li]) continue;
+        zu.push_back(FatEw{h->z + L.c0 * h->C, L.u, nullptr, L.zu, nullptr, L.nj * h->C});
+        aw.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, L.zu, L.t1, 0, L.xt});
+        kw.happly(L, L.t1, L.w0, h->prm.rho_c / h->prm.rho_l);
+    }
+    if (zu.empty()) return BICADMM_OK;
+    H_RC(h, launch_fat_ew(zu.data(), (int)zu.size(), 2, h->st));
+    H_RC(h, launch_gemv(h->dtype, aw.data(), (int)aw.size(), h->gemv_cap, h->st, h->C));
+    H_RC(h, kw.launch(h));
+    return BICADMM_OK;
+}
+
 static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
     std::vector<char> act(h->nod.size(), 0);
     for (int li : nodes) act[li] = 1;
@@ -982,8 +1020,8 @@ static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
     for (size_t k = 0; k < h->blk.size(); ++k) {
         const LBlock& L = h->blk[k];
         if (!L.fat || !act[L.li]) continue;
-        GemvTDesc g = h->gt[k];
-        g.delta = nullptr; g.z = L.r; g.u = nullptr; g.r = L.x;
+        GemvTDesc g = h->gt[k];   // x = (rho_l A^T (q - p) + rho_c (z - u)) / c
+        g.p = L.qd; g.delta = nullptr; g.r = L.x;
         gt.push_back(g);
     }
     if (gt.empty()) return BICADMM_OK;
@@ -991,7 +1029,7 @@ static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
     const int64_t l0 = g_launches.load();
     if (h->prof) { a = next_event(h); cudaEventRecord(a, h->st); }
     const double c = h->prm.lambda / (double)h->N + h->prm.rho_c;
-    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), -h->prm.rho_l / c, 1.0 / c, h->st, nullptr, h->C));
+    H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l / c, h->prm.rho_c / c, h->st, nullptr, h->C));
     if (h->prof) {
         b = next_event(h);
         cudaEventRecord(b, h->st);
@@ -1095,9 +1133,15 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
         std::vector<int> want(h->nod.size());
         int maxs = 0;
         if (!tol) {
+            std::vector<int> swept;
             for (size_t li = 0; li < h->nod.size(); ++li) {
                 want[li] = sweeps_for(h, k, (int)li);
                 maxs = std::max(maxs, want[li]);
+                if (want[li] > 0) swept.push_back((int)li);
+            }
+            if (h->any_fat) {
+                int rc = fat_prepare(h, swept);
+                if (rc) return rc;
             }
             for (int sw = 0; sw < maxs; ++sw) {
                 std::vector<int> active;
@@ -1105,8 +1149,6 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
                 int rc = inner_sweep(h, active);
                 if (rc) return rc;
             }
-            std::vector<int> swept;
-            for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > 0) swept.push_back((int)li);
             if (h->any_fat) {
                 int rc = materialize_x(h, swept);
                 if (rc) return rc;
@@ -1117,6 +1159,10 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
             std::vector<int> active;
             for (size_t li = 0; li < h->nod.size(); ++li) active.push_back((int)li);
             std::vector<double> res, dx;
+            if (h->any_fat) {
+                int rc = fat_prepare(h, active);
+                if (rc) return rc;
+            }
             for (int sw = 0; sw < h->prm.max_inner && !active.empty(); ++sw) {
                 int rc = inner_sweep(h, active, true);
                 if (!rc && h->any_fat) rc = materialize_x(h, active);

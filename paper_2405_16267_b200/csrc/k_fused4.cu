@@ -145,9 +145,9 @@ __device__ __forceinline__ void cluster_sync_all() {
 //         ring keeps nring - 1 half-rows in flight.
 template <typename T, int E, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
-    k_fused4(const Fused2Args a, int loss, double rho, int nring) {
+    k_fused4(const Fused2Args a, int loss, double rho, int nring, int dly) {
     constexpr bool L2AX = MODE == 1;
-    constexpr int D = L2AX ? kF4DL2 : kF4D;
+    const int D = L2AX ? kF4DL2 : dly;   // axpy delay (rows)
     extern __shared__ __align__(128) unsigned char f4_smem[];
     T* ring = reinterpret_cast<T*>(f4_smem);             // nring x half_pad elements
     __shared__ double dotp[kF4Q][2 * kF4Main];            // [slot][cta * 12 + warp]
@@ -405,7 +405,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                 nu0 = a.nu[nd][rl];
                 w0 = a.delta[nd][rl] + a.p[nd][rl] + nu0;
             }
-            mb4_wait_cluster(&bar_dot[q], (unsigned)(((r - rb) / kF4Q) & 1));
+            // the peer's dots arrive by st.async complete_tx on this CTA's barrier: observing the
+            // phase (CTA-scope acquire, as for TMA) makes them visible; no cluster-scope acquire
+            mb4_wait_cta(&bar_dot[q], (unsigned)(((r - rb) / kF4Q) & 1));
             double qq = 0.0;
             if (on) {
                 double p = 0.0;
@@ -444,6 +446,13 @@ static int f4_ring(const Fused2Args& a, size_t es) {
     return r > kF4RingMax ? kF4RingMax : r;
 }
 
+// axpy delay D (rows between a row's dot and its axpy; the ring holds D + 1 rows):
+// BICADMM_F4_D, default 2, at most nring - 2 so that >= 1 slot is always loading
+static int f4_delay(int nring) {
+    static int d = [] { const char* e = getenv("BICADMM_F4_D"); int v = e ? atoi(e) : kF4D; return v < 1 ? 1 : v; }();
+    return d > nring - 2 ? nring - 2 : d;
+}
+
 template <typename T, int MODE>
 static int f4_launch(int E, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
     const int nring = f4_ring(a, sizeof(T));
@@ -458,7 +467,7 @@ static int f4_launch(int E, const Fused2Args& a, int loss, double rho, int grid,
                 return BICADMM_ERR_CUDA;                                                                       \
             set = true;                                                                                        \
         }                                                                                                      \
-        k_fused4<T, EE, MODE><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring);                             \
+        k_fused4<T, EE, MODE><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring, f4_delay(nring));                             \
         break;                                                                                                 \
     }
     switch (E) {

@@ -32,7 +32,9 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
                                                      double* __restrict__ z_prev, OuterScalars* sc) {
     __shared__ double scratch[32];
     __shared__ double probe_red[32][kProbes + 1];
+    __shared__ int probe_cnt[32][kProbes + 1];
     __shared__ uint64_t s_lo, s_hi;
+    __shared__ int s_clo, s_chi, s_done;
     const double v = sc->v;
     const double Nd = (double)N, Nrc = Nd * rho_c;
     double psi0 = 0.0, sw = 0.0, bmax = 0.0;
@@ -58,33 +60,51 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
         if (Nrc * bmax + rho_b * v <= 0.0) {
             Asum = 0.0; Bsum = 0.0;   // every shrinkable coordinate is zero
         } else {
-            if (threadIdx.x == 0) { s_lo = 0; s_hi = dkey(bmax); }
+            // early exit: the closed form below depends only on the active set
+            // {l : |w_l|/d_l > tau}; once the bracket holds no breakpoint |w_l|/d_l
+            // (count(lo) == count(hi), the count is monotone in tau) that set is fixed,
+            // so stopping there gives bit-for-bit the same tau as narrowing to one ulp.
+            int c0 = 0;
+            for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+                const double w = wbar[l];
+                const double dl = 1.0 - s[l] * sgn(w);
+                c0 += (dl > 0.0 && w != 0.0 && fabs(w) / dl > 0.0);
+            }
+            c0 = (int)block_sum((double)c0, scratch);
+            if (threadIdx.x == 0) { s_lo = 0; s_hi = dkey(bmax); s_clo = c0; s_chi = 0; s_done = 0; }
             __syncthreads();
             const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
             for (int pass = 0; pass < 40; ++pass) {
                 const uint64_t lo = s_lo, hi = s_hi;
-                if (hi - lo <= 1) break;
+                if (hi - lo <= 1 || s_done) break;
                 const uint64_t d = hi - lo;
                 double tp[kProbes], acc[kProbes];
+                int cn[kProbes];
 #pragma unroll
                 for (int p = 0; p < kProbes; ++p) {
                     const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
                     tp[p] = kdbl(kp);
                     acc[p] = 0.0;
+                    cn[p] = 0;
                 }
                 for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
                     const double w = wbar[l];
                     const double dl = 1.0 - s[l] * sgn(w);
                     if (dl > 0.0) {
                         const double aw = fabs(w);
+                        const double bl = w != 0.0 ? aw / dl : -1.0;
 #pragma unroll
-                        for (int p = 0; p < kProbes; ++p) acc[p] += dl * fmax(aw - tp[p] * dl, 0.0);
+                        for (int p = 0; p < kProbes; ++p) {
+                            acc[p] += dl * fmax(aw - tp[p] * dl, 0.0);
+                            cn[p] += bl > tp[p];
+                        }
                     }
                 }
 #pragma unroll
                 for (int p = 0; p < kProbes; ++p) {
                     const double t = warp_sum(acc[p]);
-                    if (lane == 0) probe_red[wid][p] = t;
+                    const int c = __reduce_add_sync(0xffffffffu, cn[p]);
+                    if (lane == 0) { probe_red[wid][p] = t; probe_cnt[wid][p] = c; }
                 }
                 __syncthreads();
                 if (threadIdx.x == 0) {
@@ -96,12 +116,16 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
                         if (f <= 0.0) best = p;
                     }
                     uint64_t nlo = lo, nhi = hi;
+                    int clo = s_clo, chi = s_chi;
                     for (int p = 0; p < kProbes; ++p) {
                         const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
-                        if (p <= best) nlo = kp;
-                        else if (kp < nhi && kp > nlo) { nhi = kp; break; }
+                        int cp = 0;
+                        for (int ww = 0; ww < kOuterThreads / 32; ++ww) cp += probe_cnt[ww][p];
+                        if (p <= best) { nlo = kp; clo = cp; }
+                        else if (kp < nhi && kp > nlo) { nhi = kp; chi = cp; break; }
                     }
-                    s_lo = nlo; s_hi = nhi;
+                    s_lo = nlo; s_hi = nhi; s_clo = clo; s_chi = chi;
+                    s_done = clo == chi;
                 }
                 __syncthreads();
             }

@@ -128,10 +128,22 @@ __global__ void __launch_bounds__(256) k_symv_reduce(const SymvBatch B) {
     const int64_t r = e - B.elem_begin[k];
     const int64_t I = r / kTS, rr = r % kTS, nb = (D.n + kTS - 1) / kTS;
     const double* P = D.part;
-    double s = 0.0;
+    // the (nb) terms in a fixed order: J = 0..I (row dots of tile (I, J)), then
+    // K = I+1..nb-1 (column dots of tile (K, I)); loads issued 8 at a time ahead of the adds
     const int64_t row0 = I * (I + 1) / 2;
-    for (int64_t J = 0; J <= I; ++J) s += P[(row0 + J) * (2 * kTS) + rr];
-    for (int64_t K = I + 1; K < nb; ++K) s += P[(K * (K + 1) / 2 + I) * (2 * kTS) + kTS + rr];
+    auto addr = [&](int64_t q) -> const double* {
+        return q <= I ? P + (row0 + q) * (2 * kTS) + rr : P + (q * (q + 1) / 2 + I) * (2 * kTS) + kTS + rr;
+    };
+    double s = 0.0;
+    int64_t q = 0;
+    for (; q + 8 <= nb; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(addr(q + u));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; q < nb; ++q) s += __ldcg(addr(q));
     D.y[r] = D.alpha * s;
 }
 

@@ -125,4 +125,41 @@ int launch_axpy_scaled(int64_t n, double a, const double* x, double* y, cudaStre
     return BICADMM_OK;
 }
 
+// Woodbury fat-block sweep elementwise steps (R27), batched over blocks:
+//   mode 0: o = a + b                       (q = p + delta;  zu = z - u uses mode 2)
+//   mode 1: o = a + b + c, d = a - o        (p = q + t1 + y0, diff = q - p)
+//   mode 2: o = a - b
+struct FatEwBatch { FatEw d[kMaxDesc]; int64_t begin[kMaxDesc + 1]; int nd; };
+
+__global__ void k_fat_ew(const FatEwBatch B, int mode) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B.begin[B.nd]) return;
+    int k = 0;
+    while (k + 1 < B.nd && g >= B.begin[k + 1]) ++k;
+    const FatEw& e = B.d[k];
+    const int64_t l = g - B.begin[k];
+    const double a = e.a[l], b = e.b ? e.b[l] : 0.0;
+    if (mode == 0) e.o[l] = a + b;
+    else if (mode == 2) e.o[l] = a - b;
+    else {
+        const double o = (a + b) + e.c[l];
+        e.o[l] = o;
+        e.d[l] = a - o;
+    }
+}
+
+int launch_fat_ew(const FatEw* d, int nd, int mode, cudaStream_t s) {
+    for (int base = 0; base < nd; base += kMaxDesc) {
+        FatEwBatch B;
+        B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;
+        int64_t t = 0;
+        for (int k = 0; k < B.nd; ++k) { B.d[k] = d[base + k]; B.begin[k] = t; t += B.d[k].n; }
+        B.begin[B.nd] = t;
+        if (t == 0) continue;
+        k_fat_ew<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(B, mode);
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
 }  // namespace bic

@@ -188,6 +188,8 @@ int launch_cg_xr(int64_t n, const double* sc, const double* p, const double* Ap,
 int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStream_t s);
 int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s);
 int launch_support_mask(int64_t cap, const int64_t* sup, const int64_t* cnt, double* mask, cudaStream_t s);
+struct FatEw { const double* a; const double* b; const double* c; double* o; double* d; int64_t n; };
+int launch_fat_ew(const FatEw* d, int nd, int mode, cudaStream_t s);   // k_vec.cu
 int launch_axpy_into(int64_t n, const double* x, double* y, cudaStream_t s);          // y += x
 int launch_axpy_scaled(int64_t n, double a, const double* x, double* y, cudaStream_t s);  // y += a x
 
