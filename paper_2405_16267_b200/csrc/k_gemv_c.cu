@@ -166,6 +166,7 @@ static void gemv_c_dispatch(int C, unsigned g, cudaStream_t s, const GemvBatchC&
 
 int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s) {
     if (C < 2 || C > 16) return BICADMM_ERR_INVALID;
+    if (gemv_c_dmma_enabled()) return launch_gemv_c_dmma(dtype, C, d, nd, s);   // k_gemv_dmma.cu
     int rc = transpose_batch(d, nd, C, s);
     if (rc) return rc;
     for (int base = 0; base < nd; base += kMaxDesc) {
@@ -194,7 +195,7 @@ constexpr int kGtCThreads = 32 * kGtCWarps;
 // vector slots per lane: 2 x double2 (FP64) or 1 x float4 (FP32) -> 128-column strips
 template <typename T> __host__ __device__ constexpr int gtc_slots() { return sizeof(T) == 8 ? 2 : 1; }
 
-int gemv_t_c_strip_width(int dtype) { (void)dtype; return 128; }
+int gemv_t_c_strip_width(int dtype) { (void)dtype; return gemv_c_dmma_enabled() ? 256 : 128; }
 
 struct GemvTBatchC {
     GemvTDesc d[kMaxDesc];
@@ -314,6 +315,7 @@ static int gemv_t_c_dispatch(int C, unsigned g, cudaStream_t s, const GemvTBatch
 }
 
 int launch_gemv_t_c_partial(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s) {
+    if (gemv_c_dmma_enabled()) return launch_gemv_t_c_dmma(dtype, C, d, nd, s);   // k_gemv_dmma.cu
     for (int base = 0; base < nd; base += kMaxDesc) {
         GemvTBatchC B;
         B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;

@@ -33,6 +33,10 @@ int64_t symv_part_doubles(int64_t n);
 int launch_symv_packed(int dtype, const SymvDesc* d, int nd, cudaStream_t s);
 int launch_symv_pack(int dtype, int64_t n, const double* G, int64_t ldg, void* Hp, cudaStream_t s);
 int launch_gemv_c(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
+// DMMA (FP64 tensor pipe) variants for C > 1 (k_gemv_dmma.cu); BICADMM_GEMVC_DMMA=0 selects
+// the scalar-FMA kernels of k_gemv_c.cu
+bool gemv_c_dmma_enabled();
+int launch_gemv_c_dmma(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s);
 int gemv_grid_cap(int dtype, int sm_count);  // persistent grid size (resident CTAs)
 
 // r[l] = rho_l * sum_r A[r, l] (p[r] + delta[r]) + rho_c (z[l] - u[l])   (Eq. (24))
@@ -55,6 +59,7 @@ void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need, i
 int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s,
                   cudaEvent_t mid = nullptr, int C = 1);
 int launch_gemv_t_c_partial(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s);
+int launch_gemv_t_c_dmma(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s);
 int launch_gemv_t_reduce(GemvTDesc* d, int nd, double rho_l, double rho_c, cudaStream_t s, int C = 1);
 int gemv_t_c_strip_width(int dtype);
 int gemv_t_strip_width(int dtype);
