@@ -90,10 +90,11 @@ def lib() -> ct.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+    path = os.environ.get("BICADMM_LIB_PATH", LIB_PATH)   # A/B timing of alternative builds only
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with __graft_entry__.build() "
                            "(python -m paper_2405_16267_b200.build); there is no CPU fallback")
-    L = ct.CDLL(LIB_PATH)
+    L = ct.CDLL(path)
     P = ct.POINTER
     sig = {
         "bicadmm_version": (ct.c_int, []),
