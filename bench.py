@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-n", type=int, default=1_000, help="cpu_baseline sample columns")
     ap.add_argument("--sweep", type=int, default=0, help="0 auto (fused single pass), 1 two-pass, 2 fused")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance row")
+    ap.add_argument("--no-prof", action="store_true",
+                    help="no per-phase events in the timed region (launch-overhead study; roofline null)")
     ap.add_argument("--config", default="C2", choices=sorted(PRESETS),
                     help="BASELINE.json config preset (per-rank shape); C2 = configs[1] (default)")
     a = ap.parse_args()
@@ -213,7 +215,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         solver.iterate(1)
-    solver.set_profiling(True)
+    solver.set_profiling(not args.no_prof)
     launches0 = solver.launches()
     clocks = ClockSampler(local)
     if world > 1:
@@ -263,12 +265,14 @@ def run_ours(args):
         return sweeps if (k in per_sweep and v[1] > 0) else v[1]
 
     cand = {k: phases[k] for k in byt if phases[k][1] > 0}
-    dom = max(cand, key=lambda k: cand[k][0])
-    dms, dcnt = cand[dom]
-    avg_s = dms / calls(dom, cand[dom]) / 1e3
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = byt[dom] / avg_s / 1e9
+    dom, achieved = None, None
+    if cand:   # absent with --no-prof
+        dom = max(cand, key=lambda k: cand[k][0])
+        dms, dcnt = cand[dom]
+        avg_s = dms / calls(dom, cand[dom]) / 1e3
+        achieved = byt[dom] / avg_s / 1e9
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -344,9 +348,10 @@ def run_ours(args):
                        "inner_sweep": "fused single HBM pass (k_fused4: CTA-pair clusters, SURVEY 8(f)1)" if fused_mode
                        else "two-pass (GEMV-T + GEMV)",
                        "two_pass_equivalent_GBps": (2 * A_bytes + nl * n * n * s) * sweeps / (ms / 1e3) / 1e9},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
+            "roofline": None if dom is None else {
+                "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
             "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk,

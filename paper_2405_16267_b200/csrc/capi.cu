@@ -184,15 +184,28 @@ struct bicadmm_handle {
     int64_t launches0 = 0;
     std::string err;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    bool capturing = false;   // inside the stream capture of graph_outer
+    cudaStream_t cap_st = nullptr;   // private capture stream (the caller's may be the legacy stream)
     // per-phase profiling (bicadmm_set_profiling)
     bool prof = false;
     std::vector<cudaEvent_t> evpool;
     size_t evused = 0;
     struct Pending { int phase; cudaEvent_t a, b; int64_t launches; };
     std::vector<Pending> pending;
+    // CUDA graph of one outer iteration (fixed inner schedule): captured once, replayed
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        bool prof = false, failed = false;
+        int sweeps = -1;
+        int64_t launches = 0;
+        std::vector<Pending> pending;   // phase events recorded by the graph's event nodes
+    } graph;
     double phase_ms[BICADMM_NPHASE] = {};
     int64_t phase_cnt[BICADMM_NPHASE] = {};
 };
+
+// Record a phase event; inside a stream capture it becomes an event-record node.
+static void rec_event(bicadmm_handle* h, cudaEvent_t e) { record_event(e, h->st); }
 
 static cudaEvent_t next_event(bicadmm_handle* h) {
     if (h->evused == h->evpool.size()) {
@@ -869,7 +882,7 @@ static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_n
     auto mark = [&](int k) {
         if (!h->prof) return;
         ev[k] = next_event(h);
-        cudaEventRecord(ev[k], h->st);
+        rec_event(h, ev[k]);
         lc[k] = g_launches.load();
     };
     mark(0);   // r = rho_l sum_chunks partial + rho_c (z - u)   (partials from the previous fused pass)
@@ -950,7 +963,7 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     auto mark = [&](int k) {
         if (!h->prof) return;
         ev[k] = next_event(h);
-        cudaEventRecord(ev[k], h->st);
+        rec_event(h, ev[k]);
         lc[k] = g_launches.load();
     };
     mark(0);
@@ -958,7 +971,7 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     if (!gt.empty())
         H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l, h->prm.rho_c, h->st, mid, h->C));
     else if (mid)
-        cudaEventRecord(mid, h->st);
+        record_event(mid, h->st);
     const int64_t l_partial = (int64_t)(gt.size() + kMaxDesc - 1) / kMaxDesc;
     mark(2);
     if (tol)   // keep x^k for the ||x^{k+1} - x^k|| criterion
@@ -1027,12 +1040,12 @@ static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
     if (gt.empty()) return BICADMM_OK;
     cudaEvent_t a = nullptr, b = nullptr;
     const int64_t l0 = g_launches.load();
-    if (h->prof) { a = next_event(h); cudaEventRecord(a, h->st); }
+    if (h->prof) { a = next_event(h); rec_event(h, a); }
     const double c = h->prm.lambda / (double)h->N + h->prm.rho_c;
     H_RC(h, launch_gemv_t(h->dtype, gt.data(), (int)gt.size(), h->prm.rho_l / c, h->prm.rho_c / c, h->st, nullptr, h->C));
     if (h->prof) {
         b = next_event(h);
-        cudaEventRecord(b, h->st);
+        rec_event(h, b);
         h->pending.push_back({0, a, b, g_launches.load() - l0});
     }
     return BICADMM_OK;
@@ -1042,7 +1055,7 @@ static int outer_step(bicadmm_handle* h) {
     const double rho_b = h->prm.alpha * h->prm.rho_c;
     cudaEvent_t oa = nullptr, ob = nullptr;
     const int64_t lo0 = g_launches.load();
-    if (h->prof) { oa = next_event(h); cudaEventRecord(oa, h->st); }
+    if (h->prof) { oa = next_event(h); rec_event(h, oa); }
     H_RC(h, launch_wsum(h->len, h->lenp, h->x_all, h->u_all, (int)h->nod.size(), h->wsum, h->st));
     H_RC(h, allreduce(h, h->wsum, h->len, false));
     H_RC(h, launch_zt(h->len, h->N, h->prm.rho_c, rho_b, h->wsum, h->s, h->wbar, h->z, h->z_prev, h->sc, h->st));
@@ -1056,10 +1069,15 @@ static int outer_step(bicadmm_handle* h) {
     H_RC(h, launch_residuals(h->N, std::sqrt((double)h->N) * h->prm.rho_c, h->node_sq, h->sc, h->st));
     if (h->prof) {
         ob = next_event(h);
-        cudaEventRecord(ob, h->st);
+        rec_event(h, ob);
         h->pending.push_back({6, oa, ob, g_launches.load() - lo0});
     }
     H_CUDA(h, cudaMemcpyAsync(h->host_sc, h->sc, sizeof(OuterScalars), cudaMemcpyDeviceToHost, h->st));
+    return BICADMM_OK;
+}
+
+// after outer_step's work (eager or graph replay): wait for the 6 scalars
+static int outer_finish(bicadmm_handle* h) {
     H_CUDA(h, cudaStreamSynchronize(h->st));
     if (h->prof) resolve_phases(h);
     return BICADMM_OK;
@@ -1112,6 +1130,87 @@ static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std
     return BICADMM_OK;
 }
 
+// One outer iteration with a fixed per-node sweep count: Woodbury preparation, the
+// sweeps, x materialization (enqueue only; outer_step follows).
+static int enqueue_fixed(bicadmm_handle* h, const std::vector<int>& want, int maxs) {
+    std::vector<int> swept;
+    for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > 0) swept.push_back((int)li);
+    if (h->any_fat) H_RC(h, fat_prepare(h, swept));
+    for (int sw = 0; sw < maxs; ++sw) {
+        std::vector<int> active;
+        for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);
+        H_RC(h, inner_sweep(h, active));
+    }
+    if (h->any_fat) H_RC(h, materialize_x(h, swept));
+    return BICADMM_OK;
+}
+
+static bool graph_enabled() {   // BICADMM_GRAPH=0: eager launches (read per outer iteration)
+    const char* e = getenv("BICADMM_GRAPH");
+    return !(e && atoi(e) == 0);
+}
+
+// Capture (once per sweep count / profiling state) and replay one outer iteration as a
+// CUDA graph: K_in sweeps + the global step + the 96-byte D2H read of the scalars, one
+// cudaGraphLaunch instead of ~5 K_in + 8 launches.  Returns BICADMM_ERR_STATE if the
+// capture is refused (the caller then runs the same work eagerly).
+static int graph_outer(bicadmm_handle* h, const std::vector<int>& want, int maxs) {
+    auto& G = h->graph;
+    if (!G.exec || G.prof != h->prof || G.sweeps != maxs) {
+        if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
+        h->pending.clear();
+        h->evused = 0;
+        const int64_t l0 = g_launches.load();
+        if (!h->cap_st && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            G.failed = true;
+            return BICADMM_ERR_STATE;
+        }
+        cudaStream_t st0 = h->st;
+        h->st = h->cap_st;   // the graph is captured on the private stream, launched on the caller's
+        if (cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+            h->st = st0;
+            cudaGetLastError();
+            G.failed = true;
+            return BICADMM_ERR_STATE;
+        }
+        h->capturing = true;
+        int rc = enqueue_fixed(h, want, maxs);
+        if (!rc) rc = outer_step(h);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(h->st, &graph);
+        h->capturing = false;
+        h->st = st0;
+        cudaGraphExec_t exec = nullptr;
+        if (!rc && e == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+            G.exec = exec;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        const int64_t captured = g_launches.load() - l0;
+        g_launches.fetch_sub(captured);   // counted again at every replay
+        if (!G.exec) {   // refused: forget the capture and run eagerly from now on
+            if (getenv("BICADMM_GRAPH_DEBUG")) fprintf(stderr, "bicadmm: graph capture refused (rc %d, %s)\n", rc, cudaGetErrorString(e));
+            cudaGetLastError();
+            h->dead = false;
+            h->err.clear();
+            h->pending.clear();
+            h->evused = 0;
+            G.failed = true;
+            return BICADMM_ERR_STATE;
+        }
+        if (getenv("BICADMM_GRAPH_DEBUG")) fprintf(stderr, "bicadmm: captured outer-iteration graph (%lld launches)\n", (long long)captured);
+        G.launches = captured;
+        G.pending = h->pending;
+        h->pending.clear();
+        G.prof = h->prof;
+        G.sweeps = maxs;
+    }
+    H_CUDA(h, cudaGraphLaunch(G.exec, h->st));
+    g_launches.fetch_add(G.launches);
+    if (h->prof) h->pending = G.pending;
+    return BICADMM_OK;
+}
+
 static int sweeps_for(bicadmm_handle* h, int k, int li) {
     if (!h->schedule.empty()) {
         const int row = k - h->sched_start;
@@ -1132,26 +1231,23 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
         const bool tol = !replay && h->prm.inner_fixed == 0;
         std::vector<int> want(h->nod.size());
         int maxs = 0;
+        int orc = BICADMM_OK;
         if (!tol) {
-            std::vector<int> swept;
+            bool uniform = true;
             for (size_t li = 0; li < h->nod.size(); ++li) {
                 want[li] = sweeps_for(h, k, (int)li);
                 maxs = std::max(maxs, want[li]);
-                if (want[li] > 0) swept.push_back((int)li);
+                uniform = uniform && want[li] == want[0];
             }
-            if (h->any_fat) {
-                int rc = fat_prepare(h, swept);
-                if (rc) return rc;
-            }
-            for (int sw = 0; sw < maxs; ++sw) {
-                std::vector<int> active;
-                for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);
-                int rc = inner_sweep(h, active);
-                if (rc) return rc;
-            }
-            if (h->any_fat) {
-                int rc = materialize_x(h, swept);
-                if (rc) return rc;
+            // from the second outer iteration on, a fixed uniform schedule replays one CUDA graph
+            const bool use_graph = graph_enabled() && !replay && uniform && k >= 1 && !h->graph.failed;
+            static const bool gdbg = getenv("BICADMM_GRAPH_DEBUG") != nullptr;
+            if (gdbg) fprintf(stderr, "bicadmm: outer %d use_graph %d (replay %d uniform %d failed %d)\n", k, (int)use_graph,
+                              (int)replay, (int)uniform, (int)h->graph.failed);
+            orc = use_graph ? graph_outer(h, want, maxs) : BICADMM_ERR_STATE;
+            if (orc == BICADMM_ERR_STATE) {   // eager (or the capture was refused)
+                orc = enqueue_fixed(h, want, maxs);
+                if (!orc) orc = outer_step(h);
             }
         } else {
             // tolerance mode: sweep node i until ||abar - obar|| <= eps sqrt(m_i C) and
@@ -1179,8 +1275,9 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
                 active.swap(still);
                 maxs = sw + 1;
             }
+            orc = outer_step(h);
         }
-        int rc = outer_step(h);
+        int rc = orc ? orc : outer_finish(h);
         if (rc) return rc;
         const OuterScalars& s = *h->host_sc;
         h->trace.push_back({s.p_r, s.d_r, s.b_r, s.t, s.v, s.tau});
@@ -1492,6 +1589,8 @@ extern "C" int bicadmm_destroy(bicadmm_handle* h) {
     if (h->e0) cudaEventDestroy(h->e0);
     if (h->e1) cudaEventDestroy(h->e1);
     for (auto e : h->evpool) cudaEventDestroy(e);
+    if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
+    if (h->cap_st) cudaStreamDestroy(h->cap_st);
     delete h;
     return BICADMM_OK;
 }

@@ -31,6 +31,15 @@ inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_or
         if (_e != cudaSuccess) return BICADMM_ERR_CUDA;           \
     } while (0)
 
+// Record a timing event on stream s; inside a stream capture it becomes an event-record
+// node of the graph (so phase timings survive graph replay).
+inline cudaError_t record_event(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

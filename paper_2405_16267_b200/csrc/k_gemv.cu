@@ -384,7 +384,7 @@ int launch_gemv_t(int dtype, GemvTDesc* d, int nd, double rho_l, double rho_c, c
             BIC_LAUNCHED();
         }
     }
-    if (mid) BIC_CUDA(cudaEventRecord(mid, s));
+    if (mid) BIC_CUDA(record_event(mid, s));
     return launch_gemv_t_reduce(d, nd, rho_l, rho_c, s, C);
 }
 

@@ -293,3 +293,28 @@ def test_full_h_layout_matches_oracle(bc, orc):
             _check_fp64(solver, rep, zs, xs, ref, K)
     finally:
         del os.environ["BICADMM_HPACK"]
+
+
+@pytest.mark.parametrize("sweep", [1, 2], ids=["two_pass", "fused"])
+def test_graph_replay_bit_identical_to_eager(bc, sweep):
+    # one outer iteration is captured as a CUDA graph and replayed (default); the eager
+    # launches (BICADMM_GRAPH=0) must give bit-identical iterates and the same launch count
+    import os
+    P = dg.generate(3, 400, 128, 6, "logistic", seed=9)
+    cs = dg.block_partition(128, 1)
+    out = {}
+    for g in ("1", "0"):
+        os.environ["BICADMM_GRAPH"] = g
+        try:
+            s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic",
+                           bc.Params(kappa=6, max_outer=8, inner_fixed=4, eps_p=0.0, eps_d=0.0, eps_b=0.0,
+                                     sweep=sweep), cs)
+            l0 = s.launches()
+            s.iterate(6)
+            out[g] = (s.z, s.trace(), s.launches() - l0)
+            s.close()
+        finally:
+            del os.environ["BICADMM_GRAPH"]
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["1"][2] == out["0"][2]
