@@ -120,6 +120,28 @@ struct Bump {  // 256-byte aligned bump allocator over the workspace (base may b
 
 int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// Static row split of all local rows over `units` equal ranges (one per CTA or CTA pair):
+// for each node, the first unit touching it and how many units touch it.
+void touching_units(const std::vector<int64_t>& node_rows, int units, std::vector<int64_t>& lo_out,
+                    std::vector<int64_t>& n_out) {
+    const size_t nl = node_rows.size();
+    int64_t tot = 0;
+    std::vector<int64_t> off;
+    for (size_t k = 0; k < nl; ++k) { off.push_back(tot); tot += node_rows[k]; }
+    lo_out.assign(nl, 0);
+    n_out.assign(nl, 0);
+    for (size_t k = 0; k < nl; ++k) {
+        const int64_t r0 = off[k], r1 = off[k] + node_rows[k];
+        int64_t lo = -1, hi = -1;
+        for (int c = 0; c < units; ++c) {
+            const int64_t cb = (int64_t)c * tot / units, ce = (int64_t)(c + 1) * tot / units;
+            if (cb < ce && cb < r1 && ce > r0) { if (lo < 0) lo = c; hi = c; }
+        }
+        lo_out[k] = lo < 0 ? 0 : lo;
+        n_out[k] = lo < 0 ? 0 : hi - lo + 1;
+    }
+}
+
 }  // namespace
 
 struct bicadmm_handle {
@@ -436,27 +458,21 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         for (auto& L : h->blk) L.fpart = b.arr<double>(h->nod[L.li].nchunks * L.nj * C);
     }
     {   // fused v2: static row ranges of one CTA per SM; partials per node over the CTAs touching it
-        const int G = h->sm_count;
-        int64_t R = 0;
-        std::vector<int64_t> off;
-        for (auto& nd : h->nod) { off.push_back(R); R += nd.m; }
-        h->f2_cta_lo.assign(nl, 0);
-        h->f2_cta_n.assign(nl, 0);
-        for (auto& nd : h->nod) {
-            const int64_t r0 = off[nd.li], r1 = off[nd.li] + nd.m;
-            int64_t lo = -1, hi = -1;
-            for (int c = 0; c < G; ++c) {
-                const int64_t cb = (int64_t)c * R / G, ce = (int64_t)(c + 1) * R / G;
-                if (cb < ce && cb < r1 && ce > r0) { if (lo < 0) lo = c; hi = c; }
-            }
-            h->f2_cta_lo[nd.li] = lo < 0 ? 0 : lo;
-            h->f2_cta_n[nd.li] = lo < 0 ? 0 : hi - lo + 1;
-        }
+        // (v4: per CTA pair and row group -- sized for the larger of the two)
+        std::vector<int64_t> rows;
+        for (auto& nd : h->nod) rows.push_back(nd.m);
+        touching_units(rows, h->sm_count, h->f2_cta_lo, h->f2_cta_n);
+        std::vector<int64_t> lo4, n4;
+        touching_units(rows, std::max(1, h->sm_count / 2), lo4, n4);
+        int64_t maxc = 0;
+        for (auto& L : h->blk) maxc = std::max(maxc, L.nj);
+        const int64_t g4 = fused4_groups(P->dtype, maxc);
         int64_t slots = 0;
         for (auto& nd : h->nod) slots += h->f2_cta_n[nd.li];
         h->f2slots = b.arr<double>(slots);
         for (auto& L : h->blk)
-            if (L.jl == 0) L.partial2 = b.arr<double>(std::max<int64_t>(1, h->f2_cta_n[L.li]) * L.nj * C);
+            if (L.jl == 0)
+                L.partial2 = b.arr<double>(std::max<int64_t>({1, h->f2_cta_n[L.li], n4[L.li] * g4}) * L.nj * C);
     }
     h->gram = b.arr<double>(ldg * kdmax);
     h->fws = b.arr<double>((int64_t)factor_ws_doubles(kdmax));
@@ -558,22 +574,16 @@ static int build_fused2(bicadmm_handle* h) {
     Fused2Args& a = h->f2;
     a = Fused2Args{};
     int64_t R = 0, maxc = 0, slot = 0;
+    int64_t groups = 1;
     if (h->fused_kind == 4) {
-        // row ranges per CTA pair (cluster of 2): recompute the touching ranges with G/2 units
-        const int G = h->sm_count / 2;
-        int64_t tot = 0;
-        std::vector<int64_t> off;
-        for (auto& nd : h->nod) { off.push_back(tot); tot += nd.m; }
-        for (auto& nd : h->nod) {
-            const int64_t r0 = off[nd.li], r1 = off[nd.li] + nd.m;
-            int64_t lo = -1, hi = -1;
-            for (int c = 0; c < G; ++c) {
-                const int64_t cb = (int64_t)c * tot / G, ce = (int64_t)(c + 1) * tot / G;
-                if (cb < ce && cb < r1 && ce > r0) { if (lo < 0) lo = c; hi = c; }
-            }
-            h->f2_cta_lo[nd.li] = lo < 0 ? 0 : lo;
-            h->f2_cta_n[nd.li] = lo < 0 ? 0 : hi - lo + 1;
-        }
+        // row ranges per CTA pair (cluster of 2): recompute the touching ranges with G/2 units;
+        // each cluster writes one partial row per row group
+        std::vector<int64_t> rows;
+        for (auto& nd : h->nod) rows.push_back(nd.m);
+        touching_units(rows, h->sm_count / 2, h->f2_cta_lo, h->f2_cta_n);
+        int64_t mc = 0;
+        for (auto& L : h->blk) mc = std::max(mc, L.nj);
+        groups = fused4_groups(h->dtype, mc);
     }
     a.nn = (int)h->nod.size();
     for (auto& L : h->blk) {
@@ -585,7 +595,8 @@ static int build_fused2(bicadmm_handle* h) {
         slot += h->f2_cta_n[k];
         R += L.m;
         maxc = std::max(maxc, L.nj);
-        H_CUDA(h, cudaMemsetAsync(L.partial2, 0, sizeof(double) * std::max<int64_t>(1, h->f2_cta_n[k]) * L.nj, h->st));
+        H_CUDA(h, cudaMemsetAsync(L.partial2, 0, sizeof(double) * std::max<int64_t>(1, h->f2_cta_n[k] * groups) * L.nj,
+                                  h->st));
     }
     a.total_rows = R;
     a.max_cols_pad = rup(maxc, 4);
@@ -596,7 +607,7 @@ static int build_fused2(bicadmm_handle* h) {
         GemvTDesc g{};
         g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
         g.z = h->z + L.c0 * h->C; g.u = L.u; g.r = L.r; g.partial = L.partial2;
-        g.nchunks = (int32_t)std::max<int64_t>(1, h->f2_cta_n[L.li]); g.nstrips = 1; g.chunk_rows = 0;
+        g.nchunks = (int32_t)std::max<int64_t>(1, h->f2_cta_n[L.li] * groups); g.nstrips = 1; g.chunk_rows = 0;
         h->gtf.push_back(g);
     }
     return BICADMM_OK;

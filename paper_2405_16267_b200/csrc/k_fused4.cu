@@ -31,7 +31,7 @@ constexpr int kF4Main = 12;                    // main warps per CTA
 constexpr int kF4Prox = 3;                     // prox warps per CTA
 constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp = 512
 constexpr int kF4MainT = 32 * kF4Main;         // 384
-constexpr int kF4RingMax = 8;                  // half-row ring depth (runtime nring <= 8, by smem)
+constexpr int kF4RingMax = 16;                 // half-row ring depth (runtime nring <= 16, by smem)
 constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
 constexpr int kF4DL2 = 8;                      // axpy delay when the axpy re-reads the row from L2
 constexpr int kF4Q = 32;                       // dot / q slots (>= delay + lag window)
@@ -143,11 +143,16 @@ __device__ __forceinline__ void cluster_sync_all() {
 // MODE 2: each thread keeps its own columns of rows k-1, k-2 in registers (a delay
 //         line), x lives in smem, and the slot is released right after the dot -> the
 //         ring keeps nring - 1 half-rows in flight.
-template <typename T, int E, int MODE>
+template <typename T, int E, int MODE, int GR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
-    k_fused4(const Fused2Args a, int loss, double rho, int nring, int dly) {
+    k_fused4(const Fused2Args a, int loss, double rho, int nring, int dly, int ngrp) {
     constexpr bool L2AX = MODE == 1;
-    const int D = L2AX ? kF4DL2 : dly;   // axpy delay (rows)
+    const int D = L2AX ? kF4DL2 : dly;   // axpy delay (rows; in a group's own rows when ngrp > 1)
+    // row groups (MODE 0): the 12 main warps form ngrp groups of W warps; group gi owns the
+    // rows rb + gi, rb + gi + ngrp, ...  For narrow rows this overlaps the per-row latency
+    // chain of ngrp rows.  Every row's dot has W partials per CTA.
+    if (GR == 1) ngrp = 1;               // GR = 1: one group, W = 12 at compile time
+    const int W = kF4Main / ngrp;
     extern __shared__ __align__(128) unsigned char f4_smem[];
     T* ring = reinterpret_cast<T*>(f4_smem);             // nring x half_pad elements
     __shared__ double dotp[kF4Q][2 * kF4Main];            // [slot][cta * 12 + warp]
@@ -163,10 +168,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         int s = 0;
         unsigned ph = 0;
         __device__ void next(int n) { if (++s == n) { s = 0; ph ^= 1u; } }
+        __device__ void adv(int n, int g) {   // g < n
+            if (GR == 1) { next(n); return; }
+            s += g;
+            if (s >= n) { s -= n; ph ^= 1u; }
+        }
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < nring; ++s) { mb4_init(&bar_full[s], 1); mb4_init(&bar_empty[s], kF4Main); }
-        for (int s = 0; s < kF4Q; ++s) { mb4_init(&bar_dot[s], kF4Main); mb4_init(&bar_q[s], 1); }
+        for (int s = 0; s < nring; ++s) { mb4_init(&bar_full[s], 1); mb4_init(&bar_empty[s], W); }
+        for (int s = 0; s < kF4Q; ++s) { mb4_init(&bar_dot[s], W); mb4_init(&bar_q[s], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cluster_sync_all();   // barriers of both CTAs initialised before any remote arrive
@@ -288,8 +298,94 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             step(k + 1, h1);
         }
         if (a.active[nda]) flush(nda);
-    } else if (MODE != 2 && warp < kF4Main) {
-        // ------------------------------------------------------------ main warps
+    } else if (MODE == 0 && GR == 0 && warp < kF4Main) {
+        // ------------------------------------------------------------ main warps (row groups)
+        const int gi = warp / W, wig = warp % W;
+        const int GT = 32 * W;                 // threads of a group (cover a half-row)
+        const int mt = wig * 32 + lane;
+        const unsigned peer = h ^ 1u;
+        int ndd = nd0, nda = nd0;
+        double xr[E], acc[E];
+        int64_t hc0, hcn;
+        auto load_x = [&](int nd) {
+            half_range(nd, hc0, hcn);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t c = mt + (int64_t)GT * e;
+                xr[e] = c < hcn ? a.x[nd][hc0 + c] : 0.0;
+            }
+        };
+        load_x(ndd);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.0;
+        int64_t ac0, acn;
+        half_range(nda, ac0, acn);
+        auto flush = [&](int node) {   // partial row (cluster, group) of the node
+            double* out = a.partial[node] + ((clu - a.cta_lo[node]) * ngrp + gi) * a.ncols[node] + ac0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t c = mt + (int64_t)GT * e;
+                if (c < acn) out[c] = acc[e];
+                acc[e] = 0.0;
+            }
+        };
+        RingPos pd, pa;   // ring slots of this group's rows (dot side, axpy side)
+        pd.s = pa.s = gi;
+        const int64_t lag = (int64_t)D * ngrp;
+        for (int64_t k = rb + gi; k < re + lag; k += ngrp) {
+            if (k < re) {
+                const int nn2 = node_of(k, ndd);
+                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
+                const int s = pd.s;
+                mb4_wait_cta(&bar_full[s], pd.ph);
+                pd.adv(nring, ngrp);
+                const T* row = ring + s * half_pad;
+                double dot = 0.0;
+                if (a.active[ndd]) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int64_t c = mt + (int64_t)GT * e;
+                        if (c < hcn) dot = fma((double)row[c], xr[e], dot);
+                    }
+                }
+                dot = warp_sum(dot);
+                if (lane == 0) {
+                    const int q = (int)((k - rb) % kF4Q);
+                    const int idx = (int)h * W + wig;
+                    dotp[q][idx] = dot;
+                    st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
+                    if (wig == 0) mb4_expect_tx(&bar_dot[q], 8u * W);   // the peer group's W stores
+                    else mb4_arrive_local(&bar_dot[q]);
+                }
+            }
+            const int64_t ra = k - lag;
+            if (ra >= rb) {
+                const int nn2 = node_of(ra, nda);
+                if (nn2 != nda) {
+                    if (a.active[nda]) flush(nda);
+                    nda = nn2;
+                    half_range(nda, ac0, acn);
+                }
+                const int q = (int)((ra - rb) % kF4Q);
+                mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
+                const double qq = qv[q];
+                const int s = pa.s;
+                pa.adv(nring, ngrp);
+                const T* row = ring + s * half_pad;
+                if (a.active[nda]) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int64_t c = mt + (int64_t)GT * e;
+                        if (c < acn) acc[e] = fma((double)row[c], qq, acc[e]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mb4_arrive_local(&bar_empty[s]);
+            }
+        }
+        if (a.active[nda]) flush(nda);
+    } else if ((MODE == 1 || GR == 1) && warp < kF4Main) {
+        // ------------------------------------------------------------ main warps (one group)
         const int mt = threadIdx.x;
         const unsigned peer = h ^ 1u;
         int ndd = nd0, nda = nd0;
@@ -412,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             if (on) {
                 double p = 0.0;
 #pragma unroll
-                for (int w = 0; w < 2 * kF4Main; ++w) p += dotp[q][w];
+                for (int w = 0; w < 2 * W; ++w) p += dotp[q][w];
                 const double om = f4_prox(loss, rho, bl, p + nu0, w0);
                 const double nu = nu0 + p - om;
                 const double dl = om - p - nu;
@@ -446,28 +542,51 @@ static int f4_ring(const Fused2Args& a, size_t es) {
     return r > kF4RingMax ? kF4RingMax : r;
 }
 
-// axpy delay D (rows between a row's dot and its axpy; the ring holds D + 1 rows):
-// BICADMM_F4_D, default 2, at most nring - 2 so that >= 1 slot is always loading
-static int f4_delay(int nring) {
-    static int d = [] { const char* e = getenv("BICADMM_F4_D"); int v = e ? atoi(e) : kF4D; return v < 1 ? 1 : v; }();
-    return d > nring - 2 ? nring - 2 : d;
+// Row groups for narrow rows: the largest ngrp in {6, 4, 3, 2} whose W = 12/ngrp warps
+// still cover a half-row with <= 12 elements per thread (BICADMM_F4_GROUPS overrides,
+// up to 16 elements).  Measured at n = 4000 FP64: 1 group 3.30 ms, 2 groups 2.49 ms,
+// 3 groups (E = 16) 2.86 ms per sweep.
+int fused4_groups(int dtype, int64_t max_cols) {
+    (void)dtype;
+    if (f4_mode() != 0) return 1;
+    const int64_t half = (max_cols + 1) / 2 + 2;
+    int g = 1;
+    const int cand[4] = {6, 4, 3, 2};
+    for (int k = 0; k < 4; ++k)   // E <= 12 (E = 16 with runtime W spills; measured)
+        if (half <= (int64_t)32 * (kF4Main / cand[k]) * 12) { g = cand[k]; break; }
+    if (const char* e = getenv("BICADMM_F4_GROUPS")) {
+        const int v = atoi(e);
+        if (v >= 1 && kF4Main % v == 0 && half <= (int64_t)32 * (kF4Main / v) * 16) g = v;
+    }
+    return g;
 }
 
-template <typename T, int MODE>
-static int f4_launch(int E, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
+// axpy delay D (in the group's own rows; the ring holds about ngrp (D + 1) rows):
+// one group: D = 2 (measured best at C2 FP64; BICADMM_F4_D overrides); ngrp > 1: the
+// largest D that leaves 2 slots loading.  Always ngrp * D <= nring - 2.
+static int f4_delay(int nring, int ngrp) {
+    static int d = [] { const char* e = getenv("BICADMM_F4_D"); return e ? (atoi(e) < 1 ? 1 : atoi(e)) : 0; }();
+    int v = d ? d : (ngrp == 1 ? kF4D : (nring - 2) / ngrp - 1);
+    if (v < 1) v = 1;
+    while (v > 1 && ngrp * v > nring - 2) --v;
+    return v;
+}
+
+template <typename T, int MODE, int GR>
+static int f4_launch(int E, int ngrp, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
     const int nring = f4_ring(a, sizeof(T));
-    if (nring < 4) return BICADMM_ERR_INVALID;
+    if (nring < 4 || ngrp >= nring - 1) return BICADMM_ERR_INVALID;
     const size_t smem = (size_t)nring * f4_slot_bytes(a, sizeof(T)) + f4_xs_bytes(a);
 #define F4_CASE(EE)                                                                                            \
     case EE: {                                                                                                 \
         static bool set = false;                                                                               \
         if (!set) {                                                                                            \
-            if (cudaFuncSetAttribute(k_fused4<T, EE, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+            if (cudaFuncSetAttribute(k_fused4<T, EE, MODE, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                      212 * 1024) != cudaSuccess)                                               \
                 return BICADMM_ERR_CUDA;                                                                       \
             set = true;                                                                                        \
         }                                                                                                      \
-        k_fused4<T, EE, MODE><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring, f4_delay(nring));                             \
+        k_fused4<T, EE, MODE, GR><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring, f4_delay(nring, ngrp), ngrp); \
         break;                                                                                                 \
     }
     switch (E) {
@@ -482,7 +601,9 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     int64_t maxc = 0;
     for (int k = 0; k < a.nn; ++k) maxc = a.ncols[k] > maxc ? a.ncols[k] : maxc;
     const int64_t half = (maxc + 1) / 2 + 2;
-    const int64_t e = (half + kF4MainT - 1) / kF4MainT;
+    const int ngrp = fused4_groups(dtype, maxc);
+    const int64_t gt = 32 * (kF4Main / ngrp);
+    const int64_t e = (half + gt - 1) / gt;
     const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 14 ? 14 : e <= 16 ? 16 : -1;
     if (E < 0 || f4_ring(a, dtype == BICADMM_F64 ? 8 : 4) < 4 || (grid & 1)) return BICADMM_ERR_INVALID;
     for (int k = 0; k < a.nn; ++k) if (a.ncols[k] % 8) return BICADMM_ERR_INVALID;
@@ -490,11 +611,15 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     const int mode = f4_mode();
     int rc;
     if (dtype == BICADMM_F64)
-        rc = mode == 2 ? f4_launch<double, 2>(E, a, loss, rho, grid, s)
-           : mode == 1 ? f4_launch<double, 1>(E, a, loss, rho, grid, s) : f4_launch<double, 0>(E, a, loss, rho, grid, s);
+        rc = mode == 2 ? f4_launch<double, 2, 1>(E, 1, a, loss, rho, grid, s)
+           : mode == 1 ? f4_launch<double, 1, 1>(E, 1, a, loss, rho, grid, s)
+           : ngrp == 1 ? f4_launch<double, 0, 1>(E, 1, a, loss, rho, grid, s)
+                       : f4_launch<double, 0, 0>(E, ngrp, a, loss, rho, grid, s);
     else
-        rc = mode == 2 ? f4_launch<float, 2>(E, a, loss, rho, grid, s)
-           : mode == 1 ? f4_launch<float, 1>(E, a, loss, rho, grid, s) : f4_launch<float, 0>(E, a, loss, rho, grid, s);
+        rc = mode == 2 ? f4_launch<float, 2, 1>(E, 1, a, loss, rho, grid, s)
+           : mode == 1 ? f4_launch<float, 1, 1>(E, 1, a, loss, rho, grid, s)
+           : ngrp == 1 ? f4_launch<float, 0, 1>(E, 1, a, loss, rho, grid, s)
+                       : f4_launch<float, 0, 0>(E, ngrp, a, loss, rho, grid, s);
     if (rc) return rc;
     BIC_LAUNCHED();
     return BICADMM_OK;

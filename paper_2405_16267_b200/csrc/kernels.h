@@ -183,6 +183,7 @@ int fused2_max_cols(int dtype);
 int launch_fused3(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int fused4_max_cols(int dtype);
+int fused4_groups(int dtype, int64_t max_cols);   // row groups of the CTA-pair sweep (partials per group)
 int fused3_max_cols(int dtype);
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)

@@ -318,3 +318,20 @@ def test_graph_replay_bit_identical_to_eager(bc, sweep):
     assert np.array_equal(out["1"][0], out["0"][0])
     assert np.array_equal(out["1"][1], out["0"][1])
     assert out["1"][2] == out["0"][2]
+
+
+@pytest.mark.parametrize("groups", ["1", "2", "3", "4", "6"])
+def test_fused4_row_groups(bc, orc, groups):
+    # the CTA-pair sweep with its 12 main warps split into row groups (partials per group);
+    # several nodes so that node boundaries fall inside clusters
+    import os
+    os.environ["BICADMM_F4_GROUPS"] = groups
+    os.environ["BICADMM_FUSED_KIND"] = "4"
+    try:
+        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 5, 611, 496, 9, "logistic", 1, 6, 5, sweep=2)
+        for k in range(6):
+            assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, (groups, k)
+        assert solver.support().tolist() == ref["support"].tolist()
+    finally:
+        del os.environ["BICADMM_F4_GROUPS"]
+        del os.environ["BICADMM_FUSED_KIND"]
