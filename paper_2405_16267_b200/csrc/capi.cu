@@ -162,6 +162,8 @@ struct bicadmm_handle {
     double *x_all = nullptr, *u_all = nullptr, *z = nullptr, *z_prev = nullptr, *s = nullptr, *wbar = nullptr,
            *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
            *fws = nullptr, *node_obj = nullptr;
+    int fbatch = 1;                          // blocks factored together (factor_inverse_batched)
+    int64_t gram_stride = 0, fws_stride = 0; // per-job setup scratch (doubles)
     double *x_old = nullptr, *dpart = nullptr, *node_dx = nullptr, *node_res = nullptr;
     double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
     int refit_iters = 0;
@@ -474,8 +476,18 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
             if (L.jl == 0)
                 L.partial2 = b.arr<double>(std::max<int64_t>({1, h->f2_cta_n[L.li], n4[L.li] * g4}) * L.nj * C);
     }
-    h->gram = b.arr<double>(ldg * kdmax);
-    h->fws = b.arr<double>((int64_t)factor_ws_doubles(kdmax));
+    {   // setup scratch for up to 8 blocks factored in lockstep (BICADMM_FACTOR_BATCH caps it;
+        // the extra scratch is limited to ~8 GB)
+        h->gram_stride = rup(ldg * kdmax, 32);
+        h->fws_stride = rup((int64_t)factor_ws_doubles(kdmax), 32);
+        const double per_job = 8.0 * (double)(h->gram_stride + h->fws_stride);
+        int fb = (int)std::min<int64_t>(8, (int64_t)h->blk.size());
+        while (fb > 1 && per_job * (fb - 1) > 8e9) --fb;
+        if (const char* e = getenv("BICADMM_FACTOR_BATCH")) fb = std::max(1, std::min(fb, atoi(e)));
+        h->fbatch = std::max(1, fb);
+        h->gram = b.arr<double>(h->gram_stride * h->fbatch);
+        h->fws = b.arr<double>(h->fws_stride * h->fbatch);
+    }
     return b.off + 256;
 }
 
@@ -826,17 +838,25 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     // one-time block factors (a0)
     cudaEventRecord(h->e0, h->st);
     const double c = R->lambda / (double)P->N + R->rho_c;   // 1/(N gamma) + rho_c
-    for (auto& L : h->blk) {
-        const int64_t ldg = rup(L.kd, 8);
-        if (L.fat)   // K = (c/rho_l) I + A A^T  (Woodbury, R27)
-            rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, h->gram, ldg, h->st);
-        else         // F = rho_l A^T A + c I  (Eq. (24))
-            rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, h->gram, ldg, false, h->st);
-        if (!rc && L.hpack) {   // full FP64 inverse into the (consumed) Gram scratch, then pack
-            rc = factor_inverse(L.kd, h->gram, ldg, h->gram, ldg, BICADMM_F64, h->fws, h->st);
-            if (!rc) rc = launch_symv_pack(P->dtype, L.kd, h->gram, ldg, L.H, h->st);
-        } else if (!rc) {
-            rc = factor_inverse(L.kd, h->gram, ldg, L.H, L.ldh, P->dtype, h->fws, h->st);
+    for (size_t b0 = 0; b0 < h->blk.size(); b0 += h->fbatch) {
+        const int nb = (int)std::min<size_t>(h->fbatch, h->blk.size() - b0);
+        std::vector<FactorJob> jobs;
+        for (int k = 0; k < nb && !rc; ++k) {
+            LBlock& L = h->blk[b0 + k];
+            const int64_t ldg = rup(L.kd, 8);
+            double* G = h->gram + k * h->gram_stride;
+            if (L.fat)   // K = (c/rho_l) I + A A^T  (Woodbury, R27)
+                rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, G, ldg, h->st);
+            else         // F = rho_l A^T A + c I  (Eq. (24))
+                rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, G, ldg, false, h->st);
+            // packed H: the full FP64 inverse goes into the (consumed) Gram scratch, then packed
+            jobs.push_back(FactorJob{L.kd, G, ldg, L.hpack ? (void*)G : L.H, L.hpack ? ldg : L.ldh,
+                                     L.hpack ? (int)BICADMM_F64 : P->dtype, h->fws + k * h->fws_stride});
+        }
+        if (!rc) rc = factor_inverse_batched(jobs.data(), (int)jobs.size(), h->st);
+        for (int k = 0; k < nb && !rc; ++k) {
+            LBlock& L = h->blk[b0 + k];
+            if (L.hpack) rc = launch_symv_pack(P->dtype, L.kd, h->gram + k * h->gram_stride, rup(L.kd, 8), L.H, h->st);
         }
         if (rc) {
             std::string msg = rc == BICADMM_ERR_CUDA ? std::string("factor: ") + cudaGetErrorString(cudaGetLastError())

@@ -37,11 +37,22 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // A(i, k): A_KFAST -> A[i*lda + k] (stored M x K), else A[k*lda + i] (stored K x M)
 // B(k, j): B_KFAST -> B[j*ldb + k] (stored N x K), else B[k*ldb + j] (stored K x N)
+// Up to kMaxBatch independent GEMMs per launch (blockIdx.z): the setup factors all local
+// blocks of equal step count in lockstep, so the small per-step Cholesky / inverse GEMMs
+// of several blocks share one launch.
+constexpr int kMaxBatch = 8;
+struct GemmBatch {
+    GemmArgs g[kMaxBatch];
+    int n;
+};
+
 template <typename TIN, typename TOUT, bool A_KFAST, bool B_KFAST>
-__global__ void __launch_bounds__(kGemmThreads) k_gemm_dmma(const GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_dmma(const __grid_constant__ GemmBatch bt) {
     __shared__ double As[2][BK][BM + PAD];
     __shared__ double Bs[2][BK][BN + PAD];
+    const GemmArgs& g = bt.g[blockIdx.z];
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (m0 >= g.M || n0 >= g.N) return;
     if (g.lower_only && n0 > m0 + BM - 1) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
@@ -138,12 +149,26 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_dmma(const GemmArgs g) {
 }
 
 template <typename TIN, typename TOUT, bool AK, bool BK_>
-static int gemm(const GemmArgs& g, cudaStream_t s) {
-    if (g.M <= 0 || g.N <= 0) return BICADMM_OK;
-    dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
-    k_gemm_dmma<TIN, TOUT, AK, BK_><<<grid, kGemmThreads, 0, s>>>(g);
+static int gemm_batched(const GemmArgs* gs, int n, cudaStream_t s) {
+    GemmBatch bt{};
+    bt.n = 0;
+    int64_t mx = 0, nx = 0;
+    for (int k = 0; k < n; ++k) {
+        if (gs[k].M <= 0 || gs[k].N <= 0) continue;
+        bt.g[bt.n++] = gs[k];
+        mx = gs[k].M > mx ? gs[k].M : mx;
+        nx = gs[k].N > nx ? gs[k].N : nx;
+    }
+    if (bt.n == 0) return BICADMM_OK;
+    dim3 grid((unsigned)((nx + BN - 1) / BN), (unsigned)((mx + BM - 1) / BM), (unsigned)bt.n);
+    k_gemm_dmma<TIN, TOUT, AK, BK_><<<grid, kGemmThreads, 0, s>>>(bt);
     BIC_LAUNCHED();
     return BICADMM_OK;
+}
+
+template <typename TIN, typename TOUT, bool AK, bool BK_>
+static int gemm(const GemmArgs& g, cudaStream_t s) {
+    return gemm_batched<TIN, TOUT, AK, BK_>(&g, 1, s);
 }
 
 int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag,
@@ -177,8 +202,20 @@ int launch_gram_rows(int dtype, int64_t m, int64_t nj, const void* A, int64_t ld
 constexpr int NB = 64;
 constexpr int kDiagThreads = 256;
 
-__global__ void __launch_bounds__(kDiagThreads) k_chol_diag(double* F, int64_t ldf, double* Wd, int64_t ldw, int kn,
-                                                          int* info) {
+struct DiagBatch {
+    double* F[kMaxBatch];
+    double* Wd[kMaxBatch];
+    int64_t ldf[kMaxBatch], ldw[kMaxBatch];
+    int kn[kMaxBatch];
+    int* info[kMaxBatch];
+};
+
+__global__ void __launch_bounds__(kDiagThreads) k_chol_diag(const __grid_constant__ DiagBatch db) {
+    double* F = db.F[blockIdx.x];
+    double* Wd = db.Wd[blockIdx.x];
+    const int64_t ldf = db.ldf[blockIdx.x], ldw = db.ldw[blockIdx.x];
+    const int kn = db.kn[blockIdx.x];
+    int* info = db.info[blockIdx.x];
     extern __shared__ double sm[];
     double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(sm);
     double (*W)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(sm + NB * (NB + 1));
@@ -230,73 +267,131 @@ size_t factor_ws_doubles(int64_t nj) {
     return (size_t)(ld * nj + NB * ld + 8);
 }
 
-int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype, double* ws,
-                   cudaStream_t s) {
-    const int64_t ldw = round_up(nj, 8);
-    double* W = ws;                 // nj x ldw, lower triangular L^{-1}
-    double* X = ws + ldw * nj;      // NB x ldw scratch
-    int* info = reinterpret_cast<int*>(X + NB * ldw);
-    BIC_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)(ldw * nj), s));
-    BIC_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
+int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s) {
+    if (njobs <= 0) return BICADMM_OK;
+    if (njobs > kMaxBatch) {
+        for (int b = 0; b < njobs; b += kMaxBatch) {
+            const int rc = factor_inverse_batched(jobs + b, njobs - b < kMaxBatch ? njobs - b : kMaxBatch, s);
+            if (rc) return rc;
+        }
+        return BICADMM_OK;
+    }
+    const int hdtype = jobs[0].hdtype;
+    for (int k = 1; k < njobs; ++k)
+        if (jobs[k].hdtype != hdtype) return BICADMM_ERR_INVALID;
+    int64_t ldw[kMaxBatch], nblk[kMaxBatch], nblk_max = 0;
+    double *W[kMaxBatch], *X[kMaxBatch];
+    int* info[kMaxBatch];
+    for (int k = 0; k < njobs; ++k) {
+        const int64_t nj = jobs[k].n;
+        ldw[k] = round_up(nj, 8);
+        W[k] = jobs[k].ws;                  // nj x ldw, lower triangular L^{-1}
+        X[k] = jobs[k].ws + ldw[k] * nj;    // NB x ldw scratch
+        info[k] = reinterpret_cast<int*>(X[k] + NB * ldw[k]);
+        BIC_CUDA(cudaMemsetAsync(W[k], 0, sizeof(double) * (size_t)(ldw[k] * nj), s));
+        BIC_CUDA(cudaMemsetAsync(info[k], 0, sizeof(int), s));
+        nblk[k] = (nj + NB - 1) / NB;
+        nblk_max = nblk[k] > nblk_max ? nblk[k] : nblk_max;
+    }
     const size_t diag_smem = sizeof(double) * 2 * NB * (NB + 1);
     static bool attr_set = false;
     if (!attr_set) {
         BIC_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem));
         attr_set = true;
     }
-    const int64_t nblk = (nj + NB - 1) / NB;
-    // right-looking blocked Cholesky of F (lower triangle of G)
-    for (int64_t kbk = 0; kbk < nblk; ++kbk) {
-        const int64_t k0 = kbk * NB, kn = nj - k0 < NB ? nj - k0 : NB, rest = nj - k0 - kn;
-        k_chol_diag<<<1, kDiagThreads, diag_smem, s>>>(G + k0 * ldg + k0, ldg, W + k0 * ldw + k0, ldw, (int)kn, info);
+    GemmArgs ga[kMaxBatch];
+    // right-looking blocked Cholesky of F (lower triangle of G), all jobs in lockstep
+    for (int64_t kbk = 0; kbk < nblk_max; ++kbk) {
+        DiagBatch db{};
+        int nd = 0;
+        for (int k = 0; k < njobs; ++k) {
+            if (kbk >= nblk[k]) continue;
+            const int64_t k0 = kbk * NB, kn = jobs[k].n - k0 < NB ? jobs[k].n - k0 : NB;
+            db.F[nd] = jobs[k].G + k0 * jobs[k].ldg + k0; db.ldf[nd] = jobs[k].ldg;
+            db.Wd[nd] = W[k] + k0 * ldw[k] + k0; db.ldw[nd] = ldw[k];
+            db.kn[nd] = (int)kn; db.info[nd] = info[k];
+            ++nd;
+        }
+        k_chol_diag<<<nd, kDiagThreads, diag_smem, s>>>(db);
         BIC_LAUNCHED();
-        if (rest <= 0) break;
-        double* F21 = G + (k0 + kn) * ldg + k0;
-        {   // panel: L21 = F21 W_kk^T  (in place; one tile column, all K read before write)
+        int np = 0;
+        for (int k = 0; k < njobs; ++k) {   // panel: L21 = F21 W_kk^T (in place; all K read before write)
+            if (kbk >= nblk[k]) continue;
+            const int64_t k0 = kbk * NB, kn = jobs[k].n - k0 < NB ? jobs[k].n - k0 : NB, rest = jobs[k].n - k0 - kn;
+            if (rest <= 0) continue;
+            double* F21 = jobs[k].G + (k0 + kn) * jobs[k].ldg + k0;
             GemmArgs g{};
             g.M = rest; g.N = kn; g.K = kn; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
-            g.A = F21; g.lda = ldg; g.B = W + k0 * ldw + k0; g.ldb = ldw; g.C = F21; g.ldc = ldg;
-            int rc = gemm<double, double, true, true>(g, s);
-            if (rc) return rc;
+            g.A = F21; g.lda = jobs[k].ldg; g.B = W[k] + k0 * ldw[k] + k0; g.ldb = ldw[k]; g.C = F21; g.ldc = jobs[k].ldg;
+            ga[np++] = g;
         }
-        {   // trailing: F22 -= L21 L21^T (lower tiles)
+        int rc = gemm_batched<double, double, true, true>(ga, np, s);
+        if (rc) return rc;
+        np = 0;
+        for (int k = 0; k < njobs; ++k) {   // trailing: F22 -= L21 L21^T (lower tiles)
+            if (kbk >= nblk[k]) continue;
+            const int64_t k0 = kbk * NB, kn = jobs[k].n - k0 < NB ? jobs[k].n - k0 : NB, rest = jobs[k].n - k0 - kn;
+            if (rest <= 0) continue;
+            double* F21 = jobs[k].G + (k0 + kn) * jobs[k].ldg + k0;
             GemmArgs g{};
             g.M = rest; g.N = rest; g.K = kn; g.alpha = -1.0; g.beta = 1.0; g.diag = 0.0;
-            g.A = F21; g.lda = ldg; g.B = F21; g.ldb = ldg;
-            g.C = G + (k0 + kn) * ldg + (k0 + kn); g.ldc = ldg; g.lower_only = 1;
-            int rc = gemm<double, double, true, true>(g, s);
-            if (rc) return rc;
+            g.A = F21; g.lda = jobs[k].ldg; g.B = F21; g.ldb = jobs[k].ldg;
+            g.C = jobs[k].G + (k0 + kn) * jobs[k].ldg + (k0 + kn); g.ldc = jobs[k].ldg; g.lower_only = 1;
+            ga[np++] = g;
         }
+        rc = gemm_batched<double, double, true, true>(ga, np, s);
+        if (rc) return rc;
     }
     // W = L^{-1}: block row i:  W_i,<i = -W_ii (L_i,<i W_<i,<i)
-    for (int64_t ib = 1; ib < nblk; ++ib) {
-        const int64_t i0 = ib * NB, in = nj - i0 < NB ? nj - i0 : NB;
-        {
+    for (int64_t ib = 1; ib < nblk_max; ++ib) {
+        int np = 0;
+        for (int k = 0; k < njobs; ++k) {
+            if (ib >= nblk[k]) continue;
+            const int64_t i0 = ib * NB, in = jobs[k].n - i0 < NB ? jobs[k].n - i0 : NB;
             GemmArgs g{};
             g.M = in; g.N = i0; g.K = i0; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
-            g.A = G + i0 * ldg; g.lda = ldg; g.B = W; g.ldb = ldw; g.C = X; g.ldc = ldw;
-            int rc = gemm<double, double, true, false>(g, s);
-            if (rc) return rc;
+            g.A = jobs[k].G + i0 * jobs[k].ldg; g.lda = jobs[k].ldg; g.B = W[k]; g.ldb = ldw[k]; g.C = X[k];
+            g.ldc = ldw[k];
+            ga[np++] = g;
         }
-        {
+        int rc = gemm_batched<double, double, true, false>(ga, np, s);
+        if (rc) return rc;
+        np = 0;
+        for (int k = 0; k < njobs; ++k) {
+            if (ib >= nblk[k]) continue;
+            const int64_t i0 = ib * NB, in = jobs[k].n - i0 < NB ? jobs[k].n - i0 : NB;
             GemmArgs g{};
             g.M = in; g.N = i0; g.K = in; g.alpha = -1.0; g.beta = 0.0; g.diag = 0.0;
-            g.A = W + i0 * ldw + i0; g.lda = ldw; g.B = X; g.ldb = ldw; g.C = W + i0 * ldw; g.ldc = ldw;
-            int rc = gemm<double, double, true, false>(g, s);
-            if (rc) return rc;
+            g.A = W[k] + i0 * ldw[k] + i0; g.lda = ldw[k]; g.B = X[k]; g.ldb = ldw[k]; g.C = W[k] + i0 * ldw[k];
+            g.ldc = ldw[k];
+            ga[np++] = g;
         }
+        rc = gemm_batched<double, double, true, false>(ga, np, s);
+        if (rc) return rc;
     }
     // H = W^T W  (W lower: K range from max(m0, n0)); lower tiles mirrored
-    GemmArgs g{};
-    g.M = nj; g.N = nj; g.K = nj; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
-    g.A = W; g.lda = ldw; g.B = W; g.ldb = ldw; g.C = H; g.ldc = ldh;
-    g.lower_only = 1; g.mirror = 1; g.tri_k = 1;
-    int rc = dtype == BICADMM_F64 ? gemm<double, double, false, false>(g, s) : gemm<double, float, false, false>(g, s);
+    for (int k = 0; k < njobs; ++k) {
+        GemmArgs g{};
+        g.M = jobs[k].n; g.N = jobs[k].n; g.K = jobs[k].n; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+        g.A = W[k]; g.lda = ldw[k]; g.B = W[k]; g.ldb = ldw[k]; g.C = jobs[k].H; g.ldc = jobs[k].ldh;
+        g.lower_only = 1; g.mirror = 1; g.tri_k = 1;
+        ga[k] = g;
+    }
+    int rc = hdtype == BICADMM_F64 ? gemm_batched<double, double, false, false>(ga, njobs, s)
+                                   : gemm_batched<double, float, false, false>(ga, njobs, s);
     if (rc) return rc;
-    int hinfo = 0;
-    BIC_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int hinfo[kMaxBatch] = {};
+    for (int k = 0; k < njobs; ++k) BIC_CUDA(cudaMemcpyAsync(&hinfo[k], info[k], sizeof(int), cudaMemcpyDeviceToHost, s));
     BIC_CUDA(cudaStreamSynchronize(s));
-    return hinfo ? BICADMM_ERR_INVALID : BICADMM_OK;
+    for (int k = 0; k < njobs; ++k)
+        if (hinfo[k]) return BICADMM_ERR_INVALID;
+    return BICADMM_OK;
+}
+
+int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype, double* ws,
+                   cudaStream_t s) {
+    FactorJob j{nj, G, ldg, H, ldh, dtype, ws};
+    return factor_inverse_batched(&j, 1, s);
 }
 
 }  // namespace bic

@@ -94,6 +94,19 @@ int launch_gram_rows(int dtype, int64_t m, int64_t nj, const void* A, int64_t ld
 // In-place: G (nj x nj FP64, lower triangle holding F) -> H = F^{-1} written to H (dtype, ldh).
 // ws: FP64 scratch of factor_ws_doubles(nj) doubles.
 size_t factor_ws_doubles(int64_t nj);
+// One factor job: F (n x n lower, FP64, leading dim ldg; overwritten) -> H = F^{-1}
+// (full symmetric, dtype hdtype, leading dim ldh); ws = factor_ws_doubles(n) FP64 scratch.
+struct FactorJob {
+    int64_t n;
+    double* G;
+    int64_t ldg;
+    void* H;
+    int64_t ldh;
+    int hdtype;
+    double* ws;
+};
+// All jobs' blocked Cholesky / inverse steps run in lockstep, up to 8 GEMMs per launch.
+int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s);
 int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype,
                    double* ws, cudaStream_t s);
 
