@@ -154,7 +154,10 @@ typedef enum {
     BICADMM_FIELD_LAUNCHES = 11, /* int64 [1]: kernels this handle has launched so far */
     BICADMM_FIELD_PHASE_MS = 12, /* double [BICADMM_NPHASE]: device time per phase accumulated while
                                     profiling is on (CUDA events on the handle's stream) */
-    BICADMM_FIELD_PHASE_COUNT = 13 /* int64 [BICADMM_NPHASE]: kernel launches per phase while profiling */
+    BICADMM_FIELD_PHASE_COUNT = 13, /* int64 [BICADMM_NPHASE]: kernel launches per phase while profiling */
+    BICADMM_FIELD_SWEEP_KIND = 14 /* int32 [2]: inner-sweep implementation chosen at setup (0 two-pass,
+                                     1-4 single-pass kernels k_fused, k_fused2, k_fused3, k_fused4) and
+                                     the number of local Woodbury (fat) blocks */
 } bicadmm_field;
 
 /* Phases timed by bicadmm_set_profiling:

@@ -24,7 +24,8 @@ LS, LOGISTIC, SOFTMAX, HINGE = 0, 1, 2, 3
 LOSSES = {"ls": LS, "logistic": LOGISTIC, "softmax": SOFTMAX, "hinge": HINGE}
 F64, F32 = 0, 1
 (FIELD_Z, FIELD_S, FIELD_SCALARS, FIELD_X_LOCAL, FIELD_U_LOCAL, FIELD_SUPPORT, FIELD_X_FINAL,
- FIELD_TRACE, FIELD_WBAR, FIELD_NU, FIELD_INNER_COUNTS, FIELD_LAUNCHES, FIELD_PHASE_MS, FIELD_PHASE_COUNT) = range(14)
+ FIELD_TRACE, FIELD_WBAR, FIELD_NU, FIELD_INNER_COUNTS, FIELD_LAUNCHES, FIELD_PHASE_MS, FIELD_PHASE_COUNT,
+ FIELD_SWEEP_KIND) = range(15)
 NPHASE = 8
 PHASES = ("gemv_t_partial", "gemv_t_reduce", "h_apply", "gemv", "allreduce", "prox", "global_step", "fused_sweep")
 SWEEP_AUTO, SWEEP_TWO_PASS, SWEEP_FUSED = 0, 1, 2
@@ -376,6 +377,11 @@ class BiCADMM:
         ms = self.get(FIELD_PHASE_MS)
         cnt = self.get(FIELD_PHASE_COUNT, np.int64)
         return {name: (float(ms[k]), int(cnt[k])) for k, name in enumerate(PHASES)}
+
+    def sweep_kind(self) -> tuple:
+        """(inner-sweep implementation: 0 two-pass, 1-4 single-pass kernels; local fat blocks)."""
+        k = self.get(FIELD_SWEEP_KIND, np.int32)
+        return int(k[0]), int(k[1])
 
     def launches(self) -> int:
         return int(self.get(FIELD_LAUNCHES, np.int64)[0])

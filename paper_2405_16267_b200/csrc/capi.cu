@@ -208,6 +208,7 @@ struct bicadmm_handle {
     int64_t launches0 = 0;
     std::string err;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int32_t host_i32[2] = {};
     bool capturing = false;   // inside the stream capture of graph_outer
     cudaStream_t cap_st = nullptr;   // private capture stream (the caller's may be the legacy stream)
     // per-phase profiling (bicadmm_set_profiling)
@@ -577,7 +578,9 @@ static bool fused2_eligible(bicadmm_handle* h, int kind = 2) {
     for (auto& nd : h->nod) if (nd.np != 1) return false;
     const int64_t cap = kind == 4 ? fused4_max_cols(h->dtype) : kind == 3 ? fused3_max_cols(h->dtype)
                                                                             : fused2_max_cols(h->dtype);
-    for (auto& L : h->blk) if (L.fat || L.nj > cap || (kind == 4 && L.nj % 8)) return false;
+    const int64_t es = h->dtype == BICADMM_F64 ? 8 : 4;
+    for (auto& L : h->blk)
+        if (L.fat || L.nj > cap || (kind == 4 && (L.nj < 8 || (L.nj * es) % 16 || (L.lda * es) % 16))) return false;
     if (kind == 4 && h->sm_count < 2) return false;
     return true;
 }
@@ -1582,6 +1585,13 @@ extern "C" int bicadmm_get(bicadmm_handle* h, int field, void* dst, size_t bytes
     case BICADMM_FIELD_PHASE_COUNT:
         sz = sizeof(int64_t) * BICADMM_NPHASE; src = h->phase_cnt; host_src = true;
         break;
+    case BICADMM_FIELD_SWEEP_KIND: {
+        h->host_i32[0] = h->fused_kind;
+        h->host_i32[1] = 0;
+        for (auto& L : h->blk) h->host_i32[1] += L.fat ? 1 : 0;
+        sz = sizeof(int32_t) * 2; src = h->host_i32; host_src = true;
+        break;
+    }
     default: return fail(h, BICADMM_ERR_INVALID, "unknown field");
     }
     if (bytes_out) *bytes_out = sz;

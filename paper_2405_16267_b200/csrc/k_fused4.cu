@@ -186,7 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         while (k + 1 < a.nn && r >= a.row_off[k + 1]) ++k;
         return k;
     };
-    // column split of node nd (ncols % 8 == 0): half 0 = [0, ch), half 1 = [ch, ncols), ch % 4 == 0,
+    // column split of node nd (ncols * sizeof(T) % 16 == 0): half 0 = [0, ch), half 1 = [ch, ncols), ch % 4 == 0,
     // so both halves start 16-byte aligned and are whole 16-byte multiples (TMA bulk copy)
     auto half_range = [&](int nd, int64_t& c0, int64_t& cn) {
         const int64_t nc = a.ncols[nd];
@@ -606,7 +606,10 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     const int64_t e = (half + gt - 1) / gt;
     const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 14 ? 14 : e <= 16 ? 16 : -1;
     if (E < 0 || f4_ring(a, dtype == BICADMM_F64 ? 8 : 4) < 4 || (grid & 1)) return BICADMM_ERR_INVALID;
-    for (int k = 0; k < a.nn; ++k) if (a.ncols[k] % 8) return BICADMM_ERR_INVALID;
+    // TMA bulk copies: both half-rows start 16-byte aligned (ch % 4 == 0, lda * size % 16 == 0)
+    // and are whole 16-byte multiples
+    const int64_t es = dtype == BICADMM_F64 ? 8 : 4;
+    for (int k = 0; k < a.nn; ++k) if ((a.ncols[k] * es) % 16 || (a.lda[k] * es) % 16) return BICADMM_ERR_INVALID;
     // BICADMM_F4_MODE: 0 (default) ring-held rows, 1 L2 re-read, 2 register delay line
     const int mode = f4_mode();
     int rc;

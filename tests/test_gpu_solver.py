@@ -210,6 +210,7 @@ def test_fused_kinds_single_block(bc, orc, kind):
         for dtype, tol in ((torch.float64, 1e-9), (torch.float32, 1e-4)):
             n = 304 if kind == "4" else 301     # the CTA-pair kernel needs n % 8 == 0
             solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 777, n, 9, "logistic", 1, 6, 5, sweep=2, dtype=dtype)
+            assert solver.sweep_kind()[0] == int(kind)
             for k in range(6):
                 assert _rel(zs[k], ref["z_trace"][k]) <= tol, (kind, dtype, k)
             assert solver.support().tolist() == ref["support"].tolist()
@@ -237,6 +238,7 @@ def test_woodbury_fat_blocks_match_oracle(bc, orc, case):
     C = case[9] if len(case) > 9 else 1
     assert m < max(np.diff(dg.block_partition(n, M)))    # at least one block takes the fat path
     solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, sweep=1)
+    assert solver.sweep_kind()[1] >= 1
     _check_fp64(solver, rep, zs, xs, ref, K)
 
 
@@ -329,9 +331,35 @@ def test_fused4_row_groups(bc, orc, groups):
     os.environ["BICADMM_FUSED_KIND"] = "4"
     try:
         solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 5, 611, 496, 9, "logistic", 1, 6, 5, sweep=2)
+        assert solver.sweep_kind() == (4, 0)
         for k in range(6):
             assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, (groups, k)
         assert solver.support().tolist() == ref["support"].tolist()
     finally:
         del os.environ["BICADMM_F4_GROUPS"]
         del os.environ["BICADMM_FUSED_KIND"]
+
+
+def test_fused4_ragged_width(bc, orc):
+    # n_j = 306 (FP64: 2448-byte rows, not a multiple of 64 bytes) on the CTA-pair kernel
+    import os
+    os.environ["BICADMM_FUSED_KIND"] = "4"
+    try:
+        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 700, 306, 9, "logistic", 1, 6, 5, sweep=2)
+        assert solver.sweep_kind() == (4, 0)
+        for k in range(6):
+            assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, k
+        assert solver.support().tolist() == ref["support"].tolist()
+    finally:
+        del os.environ["BICADMM_FUSED_KIND"]
+
+
+def test_auto_sweep_choice(bc):
+    # sweep = 0: the CTA-pair single-pass kernel for rows >= 24 KB (C = 1, single-block
+    # nodes), two-pass otherwise
+    for n, want in ((3072, 4), (2048, 0)):
+        P = dg.generate(2, 4000, n, 10, "logistic", seed=2)   # tall blocks (m_i > n_j)
+        s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(kappa=10),
+                       dg.block_partition(n, 1))
+        assert s.sweep_kind() == (want, 0), (n, s.sweep_kind())
+        s.close()
