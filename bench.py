@@ -82,6 +82,10 @@ PRESETS = {
     "C4": dict(nodes=1, m=500_000, n=20_000, kappa=500, loss="softmax", C=10, M=8, inner=5,
                workload="configs[3] at G=1: sparse softmax, C=10 classes, N=1 node x m=500k, n=20k, kappa=500, "
                         "M=8 feature blocks on one GPU, FP64, K_in=5 (A = 80 GB)"),
+    "C5s": dict(nodes=8, m=250_000, n=6_250, kappa=125, loss="hinge", C=1, M=1, inner=5,
+                workload="configs[4] per-GPU shard (block-major placement: GPU g holds block g of all 8 "
+                         "nodes): sparse hinge, 8 nodes x m_i=250k x n_j=6,250, FP64, K_in=5 (A = 100 GB); the "
+                         "cross-GPU block-sum AllReduce is absent on one GPU"),
     "C3s": dict(nodes=1, m=1_000_000, n=12_500, kappa=125, loss="ls", C=1, M=1, inner=5,
                 workload="configs[2] per-GPU shard: sparse LS, m=1M rows x n_j=12.5k (one of the 8 feature blocks; "
                          "the cross-GPU block-sum AllReduce is absent on one GPU), FP64, K_in=5 (A = 100 GB)"),
@@ -188,13 +192,13 @@ def run_ours(args):
     n, m, C, M = args.n, args.m, args.C, args.M
     cs = dg.block_partition(n, M)
     P = dg.generate(nl, m, n, args.kappa, args.loss, C=C, seed=1000 + rank, device="cuda", dtype=dtype)
-    if n % 4:   # rows must start 16-byte aligned (lda % 4 == 0): pad the node matrices (configs[0])
-        padded = []
-        for a in P.A:
-            t = torch.zeros(a.shape[0], -(-n // 4) * 4, dtype=a.dtype, device=a.device)
-            t[:, :n] = a
-            padded.append(t)
-        P.A = padded
+    if n % 4:   # rows must start 16-byte aligned (lda % 4 == 0): pad the node matrices, one at a time
+        for k in range(len(P.A)):
+            t = torch.zeros(P.A[k].shape[0], -(-n // 4) * 4, dtype=P.A[k].dtype, device=P.A[k].device)
+            t[:, :n] = P.A[k]
+            P.A[k] = t
+            del t
+            torch.cuda.empty_cache()
     comm = None
     if world > 1:
         uid = [bc.bicadmm_get_unique_id() if rank == 0 else None]
