@@ -288,8 +288,180 @@ __global__ void __launch_bounds__(kGtdThreads, 2) k_gemv_t_dmma(const __grid_con
     }
 }
 
+// ----------------------------------------------------------------------------- GEMV-T, TMA-staged
+// FP64, even C and even row widths: the CTA's A rows (32 x 256-column strip per stage) and
+// the matching p / delta slices are moved by cp.async.bulk into a 3-stage shared-memory
+// ring (one producer warp, mbarrier complete_tx), so ~200 KB per SM are in flight without
+// spending registers on it.  Rows are padded to 260 doubles: with the column mapping
+// g + 8j of the DMMA M-index, the 16 lanes of a half-warp read 4 rows x 32 contiguous
+// bytes each, 32 bytes apart modulo 128 (conflict-free).
+constexpr int kTtW = 256, kTtRS = 32, kTtLD = 260, kTtST = 3;
+constexpr int kTtThreads = 288;   // 8 consumer warps + 1 producer warp
+constexpr size_t kTtSmem = sizeof(double) * (size_t)kTtST * kTtRS * (kTtLD + 2 * 16);
+
+__device__ __forceinline__ unsigned tt_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tt_bulk(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tt_smem(dst)),
+                 "l"(src), "r"(bytes), "r"(tt_smem(bar))
+                 : "memory");
+}
+__device__ __forceinline__ bool tt_try(uint64_t* b, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(ok) : "r"(tt_smem(b)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tt_wait(uint64_t* b, unsigned parity) {
+    for (long long it = 0; !tt_try(b, parity); ++it)
+        if (it > (1ll << 26)) asm volatile("trap;");
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_constant__ GemvTBatchD B, int C) {
+    extern __shared__ __align__(128) unsigned char tt_sm[];
+    double* As = reinterpret_cast<double*>(tt_sm);        // [ST][RS][LD]
+    double* Ps = As + (size_t)kTtST * kTtRS * kTtLD;       // [ST][RS * C] (C <= 16)
+    double* Ds = Ps + (size_t)kTtST * kTtRS * 16;
+    __shared__ __align__(8) uint64_t full[kTtST], empty[kTtST];
+    const int64_t cta = blockIdx.x;
+    int di = 0;
+    while (di + 1 < B.nd && cta >= B.d[di + 1].cta_begin) ++di;
+    const GemvTDesc& D = B.d[di];
+    const int64_t local = cta - D.cta_begin;
+    const int strip = (int)(local % D.nstrips);
+    const int64_t chunk = local / D.nstrips;
+    const int64_t l0 = (int64_t)strip * kTtW, cols = D.cols;
+    const int wcols = (int)(cols - l0 < kTtW ? cols - l0 : kTtW);
+    const int64_t rb = chunk * D.chunk_rows;
+    const int64_t re = rb + D.chunk_rows < D.rows ? rb + D.chunk_rows : D.rows;
+    const int nstage = (int)((re - rb + kTtRS - 1) / kTtRS);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTtST; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tt_smem(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tt_smem(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        if (lane == 0) {
+            const double* A = static_cast<const double*>(D.A);
+            for (int st = 0; st < nstage; ++st) {
+                const int s = st % kTtST;
+                if (st >= kTtST) tt_wait(&empty[s], (unsigned)((st / kTtST - 1) & 1));
+                const int64_t r0 = rb + (int64_t)st * kTtRS;
+                const int nr = (int)(re - r0 < kTtRS ? re - r0 : kTtRS);
+                const unsigned abytes = (unsigned)(wcols * 8), vbytes = (unsigned)(nr * C * 8);
+                const unsigned total = abytes * nr + vbytes * (D.delta ? 2u : 1u);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tt_smem(&full[s])),
+                             "r"(total) : "memory");
+                double* as = As + (size_t)s * kTtRS * kTtLD;
+                for (int i = 0; i < nr; ++i) tt_bulk(as + i * kTtLD, A + (r0 + i) * D.lda + l0, abytes, &full[s]);
+                tt_bulk(Ps + (size_t)s * kTtRS * 16, D.p + r0 * C, vbytes, &full[s]);
+                if (D.delta) tt_bulk(Ds + (size_t)s * kTtRS * 16, D.delta + r0 * C, vbytes, &full[s]);
+            }
+        }
+        return;
+    }
+    const int g = lane >> 2, t = lane & 3;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[j][nt][0] = acc[j][nt][1] = 0.0;
+    const int cbase = 32 * warp + g;   // this thread's columns cbase + 8j
+    for (int st = 0; st < nstage; ++st) {
+        const int s = st % kTtST;
+        tt_wait(&full[s], (unsigned)((st / kTtST) & 1));
+        const int64_t r0 = rb + (int64_t)st * kTtRS;
+        const int nr = (int)(re - r0 < kTtRS ? re - r0 : kTtRS);
+        const double* as = As + (size_t)s * kTtRS * kTtLD;
+        const double* ps = Ps + (size_t)s * kTtRS * 16;
+        const double* ds = Ds + (size_t)s * kTtRS * 16;
+#pragma unroll
+        for (int u = 0; u < kTtRS / 4; ++u) {
+            const int i = 4 * u + t;
+            const bool ok = i < nr;
+            double a[4], q[NT];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = cbase + 8 * j;
+                a[j] = (ok && c < wcols) ? as[i * kTtLD + c] : 0.0;
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const int c = nt * 8 + g;
+                q[nt] = (ok && c < C) ? ps[i * C + c] + (D.delta ? ds[i * C + c] : 0.0) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(acc[j][nt], a[j], q[nt]);
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(
+                                        tt_smem(&empty[s])) : "memory");
+    }
+    // D[g][2t+e] of DMMA j: column l0 + 32 warp + g + 8j, class nt*8 + 2t + e
+    double* out = D.partial + chunk * cols * C;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = cbase + 8 * j;
+        if (c >= wcols) continue;
+        const int64_t l = l0 + c;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int k = nt * 8 + 2 * t + e;
+                if (k < C) out[l * C + k] = acc[j][nt][e];
+            }
+    }
+}
+
+static bool gemv_t_tma_ok(int dtype, int C, const GemvTDesc* d, int nd) {
+    static const bool on = [] { const char* e = getenv("BICADMM_GEMVTC_TMA"); return !(e && atoi(e) == 0); }();
+    if (!on || dtype != BICADMM_F64 || (C & 1)) return false;
+    for (int k = 0; k < nd; ++k)
+        if ((d[k].cols & 1) || (d[k].lda & 1) ||
+            (reinterpret_cast<uintptr_t>(d[k].A) & 15) || (reinterpret_cast<uintptr_t>(d[k].p) & 15) ||
+            (d[k].delta && (reinterpret_cast<uintptr_t>(d[k].delta) & 15)))
+            return false;
+    return true;
+}
+
 int launch_gemv_t_c_dmma(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s) {
     if (C < 2 || C > 16) return BICADMM_ERR_INVALID;
+    if (gemv_t_tma_ok(dtype, C, d, nd)) {
+        static bool attr = false;
+        if (!attr) {
+            if (cudaFuncSetAttribute(k_gemv_t_dmma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTtSmem) !=
+                    cudaSuccess ||
+                cudaFuncSetAttribute(k_gemv_t_dmma_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTtSmem) !=
+                    cudaSuccess)
+                return BICADMM_ERR_CUDA;
+            attr = true;
+        }
+        for (int base = 0; base < nd; base += kMaxDesc) {
+            GemvTBatchD B;
+            B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;
+            int64_t t = 0;
+            for (int k = 0; k < B.nd; ++k) {
+                B.d[k] = d[base + k];
+                B.d[k].cta_begin = t;
+                t += (int64_t)B.d[k].nstrips * B.d[k].nchunks;
+            }
+            B.total_ctas = t;
+            if (t == 0) continue;
+            if (C <= 8) k_gemv_t_dmma_tma<1><<<(unsigned)t, kTtThreads, kTtSmem, s>>>(B, C);
+            else k_gemv_t_dmma_tma<2><<<(unsigned)t, kTtThreads, kTtSmem, s>>>(B, C);
+            BIC_LAUNCHED();
+        }
+        return BICADMM_OK;
+    }
     for (int base = 0; base < nd; base += kMaxDesc) {
         GemvTBatchD B;
         B.nd = nd - base < kMaxDesc ? nd - base : kMaxDesc;
