@@ -95,6 +95,7 @@ def lib() -> ct.CDLL:
         L.orc_prox_direct_ls.argtypes = [_i64, _i64, _pd, _pd, _f64, _f64, _pd, _pd, _pd]
         L.orc_ridge_dense.argtypes = [ct.POINTER(_Problem), _f64, _pd]
         L.orc_refit_ls.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pd]
+        L.orc_refit_logistic.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pd]
         L.orc_best_subset.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pi64, _pd, _pd]
         _lib = L
     return _lib
@@ -343,6 +344,15 @@ def refit_ls(problem: Problem, gamma: float, T) -> np.ndarray:
     x = np.zeros(T.size)
     ps = problem.struct()
     _rc(lib().orc_refit_ls(ct.byref(ps), gamma, T.size, T.ctypes.data_as(_pi64), _d(x)))
+    return x
+
+
+def refit_logistic(problem: Problem, gamma: float, T, x0) -> np.ndarray:
+    """Logistic refit on support T (DESIGN R29), damped Newton from x0."""
+    T = np.ascontiguousarray(T, dtype=np.int64)
+    x = np.ascontiguousarray(x0, dtype=np.float64).copy()
+    ps = problem.struct()
+    _rc(lib().orc_refit_logistic(ct.byref(ps), gamma, T.size, T.ctypes.data_as(_pi64), _d(x)))
     return x
 
 

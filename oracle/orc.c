@@ -676,6 +676,12 @@ int orc_run(const orc_problem* pb, const orc_params* pr, const int32_t* schedule
             rc = orc_refit_ls(pb, pr->gamma, T, sup, xt);
             for (int64_t a = 0; a < T; ++a) res->x_final[sup[a]] = xt[a];
             free(xt);
+        } else if (pr->refit && pb->loss == ORC_LOGISTIC && T > 0) {
+            double* xt = (double*)malloc(sizeof(double) * (size_t)T);
+            for (int64_t a = 0; a < T; ++a) xt[a] = z[sup[a]];   /* start at z on T */
+            rc = orc_refit_logistic(pb, pr->gamma, T, sup, xt);
+            for (int64_t a = 0; a < T; ++a) res->x_final[sup[a]] = xt[a];
+            free(xt);
         } else {
             for (int64_t a = 0; a < T; ++a) res->x_final[sup[a]] = z[sup[a]];
         }
@@ -773,6 +779,80 @@ int orc_refit_ls(const orc_problem* pb, double gamma, int64_t k, const int64_t* 
     }
     int rc = spd_solve(k, F, x);
     free(F);
+    return rc;
+}
+
+/* Logistic refit on support T (DESIGN R29): minimise the objective (1) restricted to T,
+ *   f(x_T) = sum_i sum_r ln(1 + exp(-b_r (A_iT x_T)_r)) + ||x_T||^2 / (2 gamma),
+ * by Newton's method with the exact k x k Hessian sum_i A_iT^T diag(s(1-s)) A_iT + I/gamma
+ * (s = sigma(b w)), Cholesky solves, and Armijo backtracking on f (factor 1/2, c = 1e-4).
+ * x holds the start on entry (z on T) and the minimiser on exit; stops when the Newton
+ * step's max-norm is <= 1e-13 max(1, ||x||_inf) (at most 100 steps). */
+static double logistic_refit_f(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, const double* x) {
+    double f = 0.0;
+    for (int i = 0; i < pb->N; ++i)
+        for (int64_t r = 0; r < pb->m[i]; ++r) {
+            double w = 0.0;
+            for (int64_t a = 0; a < k; ++a) w += pb->A[i][r * pb->n + T[a]] * x[a];
+            const double y = -pb->b[i][r] * w;   /* ln(1 + e^y), stable */
+            f += y > 0.0 ? y + log1p(exp(-y)) : log1p(exp(y));
+        }
+    double xx = 0.0;
+    for (int64_t a = 0; a < k; ++a) xx += x[a] * x[a];
+    return f + xx / (2.0 * gamma);
+}
+
+int orc_refit_logistic(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x) {
+    if (pb->loss != ORC_LOGISTIC || pb->C != 1) return ORC_ERR_INVALID;
+    double* F = (double*)malloc(sizeof(double) * (size_t)(k * k + 1));
+    double* g = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double* d = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double* xn = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    int rc = ORC_OK;
+    double f = logistic_refit_f(pb, gamma, k, T, x);
+    for (int it = 0; it < 100 && rc == ORC_OK; ++it) {
+        for (int64_t a = 0; a < k; ++a) g[a] = x[a] / gamma;
+        for (int64_t a = 0; a < k * k; ++a) F[a] = 0.0;
+        for (int64_t a = 0; a < k; ++a) F[a * k + a] = 1.0 / gamma;
+        for (int i = 0; i < pb->N; ++i)
+            for (int64_t r = 0; r < pb->m[i]; ++r) {
+                const double* row = pb->A[i] + r * pb->n;
+                double w = 0.0;
+                for (int64_t a = 0; a < k; ++a) w += row[T[a]] * x[a];
+                const double b = pb->b[i][r];
+                const double sp = 1.0 / (1.0 + exp(-b * w));   /* sigma(b w) */
+                const double psi = -b * (1.0 - sp);             /* d/dw ln(1 + e^{-b w}) */
+                const double dd = sp * (1.0 - sp);              /* d2/dw2 */
+                for (int64_t a = 0; a < k; ++a) {
+                    g[a] += row[T[a]] * psi;
+                    for (int64_t c = 0; c <= a; ++c) F[a * k + c] += row[T[a]] * dd * row[T[c]];
+                }
+            }
+        for (int64_t a = 0; a < k; ++a)
+            for (int64_t c = 0; c < a; ++c) F[c * k + a] = F[a * k + c];
+        for (int64_t a = 0; a < k; ++a) d[a] = -g[a];
+        rc = spd_solve(k, F, d);
+        if (rc != ORC_OK) break;
+        double gd = 0.0, dmax = 0.0, xmax = 1.0;
+        for (int64_t a = 0; a < k; ++a) {
+            gd += g[a] * d[a];
+            dmax = fmax(dmax, fabs(d[a]));
+            xmax = fmax(xmax, fabs(x[a]));
+        }
+        if (dmax <= 1e-13 * xmax) {   /* converged: take the last (tiny) step */
+            for (int64_t a = 0; a < k; ++a) x[a] += d[a];
+            break;
+        }
+        double alpha = 1.0, fn = f;
+        for (int ls = 0; ls < 60; ++ls, alpha *= 0.5) {
+            for (int64_t a = 0; a < k; ++a) xn[a] = x[a] + alpha * d[a];
+            fn = logistic_refit_f(pb, gamma, k, T, xn);
+            if (fn <= f + 1e-4 * alpha * gd) break;
+        }
+        memcpy(x, xn, sizeof(double) * (size_t)k);
+        f = fn;
+    }
+    free(F); free(g); free(d); free(xn);
     return rc;
 }
 

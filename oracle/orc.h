@@ -102,6 +102,8 @@ int orc_prox_direct_ls(int64_t m, int64_t n, const double* A, const double* b, d
                        double c, const double* z, const double* u, double* x);
 int orc_ridge_dense(const orc_problem* pb, double gamma, double* x);
 int orc_refit_ls(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x);
+/* Logistic refit on T by damped Newton (DESIGN R29); x: start (z on T) in, minimiser out. */
+int orc_refit_logistic(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x);
 int orc_best_subset(const orc_problem* pb, double gamma, int64_t kappa,
                     int64_t* support, int64_t* support_len, double* x, double* objective);
 

@@ -431,3 +431,46 @@ def test_prox_direct_ls_spec(orc):
     x = orc.prox_direct_ls(A, b, rho_c, c, z, u)
     grad = 2 * A.T @ (A @ x - b) + x / (N * gamma) + rho_c * (x - z + u)
     assert np.max(np.abs(grad)) <= 1e-10
+
+
+def _logistic_refit_problem(seed, N=2, m=80, n=14):
+    rng = np.random.default_rng(seed)
+    A = [rng.normal(size=(m, n)) / np.sqrt(m) for _ in range(N)]
+    xt = np.zeros(n)
+    xt[[1, 4, 9]] = [1.5, -2.0, 1.0]
+    b = [np.where(a @ xt + 0.3 * rng.normal(size=m) >= 0, 1.0, -1.0) for a in A]
+    return A, b
+
+
+@pytest.mark.parametrize("gamma", [100.0, 0.5])
+def test_refit_logistic_matches_scipy(orc, gamma):
+    # DESIGN R29: the refit minimises objective (1) restricted to T; pinned against an
+    # independent minimiser (scipy BFGS on the objective written with numpy) and KKT
+    A, b = _logistic_refit_problem(5)
+    T = np.array([1, 4, 7, 9])
+    pb = orc.Problem(A, b, orc.LOGISTIC, 1, np.array([0, 14]))
+
+    def f(x):
+        return sum(np.logaddexp(0.0, -bb * (a[:, T] @ x)).sum() for a, bb in zip(A, b)) + x @ x / (2 * gamma)
+
+    def g(x):
+        return sum(a[:, T].T @ (-bb / (1.0 + np.exp(bb * (a[:, T] @ x)))) for a, bb in zip(A, b)) + x / gamma
+
+    ref = optimize.minimize(f, np.zeros(T.size), jac=g, method="BFGS", options={"gtol": 1e-13, "maxiter": 10000})
+    x = orc.refit_logistic(pb, gamma, T, np.zeros(T.size))
+    assert np.max(np.abs(g(x))) <= 1e-11
+    assert np.max(np.abs(x - ref.x)) <= 1e-7 * max(1.0, np.max(np.abs(ref.x)))
+    # a far start (saturated margins) still converges to the same point: the line search
+    x2 = orc.refit_logistic(pb, gamma, T, np.array([40.0, -40.0, 40.0, -40.0]))
+    assert np.max(np.abs(x2 - x)) <= 1e-10 * max(1.0, np.max(np.abs(x)))
+
+
+def test_run_logistic_refit_is_refit_of_z(orc):
+    # orc_run with refit: x_final = refit_logistic started at z on the support
+    A, b = _logistic_refit_problem(6, N=3, m=60, n=14)
+    pb = orc.Problem(A, b, orc.LOGISTIC, 1, np.array([0, 14]))
+    r = orc.run(pb, orc.Params(kappa=3, max_outer=60, inner_fixed=5, refit=1))
+    T = r["support"]
+    x = orc.refit_logistic(pb, 100.0, T, r["z"][T])
+    assert np.allclose(r["x_final"][T], x, rtol=0, atol=1e-12)
+    assert np.count_nonzero(r["x_final"]) <= 3
