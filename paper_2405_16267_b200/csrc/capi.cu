@@ -163,6 +163,13 @@ struct bicadmm_handle {
            *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
            *fws = nullptr, *node_obj = nullptr;
     int fbatch = 1;                          // blocks factored together (factor_inverse_batched)
+    // logistic refit on the support (DESIGN R29): gathered support columns and Newton scratch
+    int64_t rf_kp = 0, rf_rows = 0, rf_nparts = 0;
+    double *rf_AT = nullptr, *rf_BT = nullptr, *rf_b = nullptr, *rf_w = nullptr, *rf_psi = nullptr,
+           *rf_sd = nullptr, *rf_obj = nullptr, *rf_x = nullptr, *rf_g = nullptr, *rf_d = nullptr,
+           *rf_F = nullptr, *rf_H = nullptr, *rf_ws = nullptr, *rf_part = nullptr, *rf_r = nullptr;
+    GemvTDesc rf_gt{};
+    int rf_newton = 0;
     int64_t gram_stride = 0, fws_stride = 0; // per-job setup scratch (doubles)
     double *x_old = nullptr, *dpart = nullptr, *node_dx = nullptr, *node_res = nullptr;
     double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
@@ -423,6 +430,35 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     // setup scratch: FP64 Gram / factor workspace
     const int64_t ldg = rup(kdmax, 8);
     h->mask = b.arr<double>(len);
+    if (P->loss == BICADMM_LOGISTIC && C == 1 && h->prm.refit) {
+        int64_t rows = 0;
+        for (auto& nd : h->nod) rows += nd.m;
+        const int64_t kk = std::max<int64_t>(1, std::min<int64_t>(h->prm.kappa, len));
+        const int64_t kp = rup(kk, 4);
+        h->rf_kp = kp;
+        h->rf_rows = rows;
+        h->rf_nparts = rf_logit_parts(rows);
+        h->rf_AT = b.arr<double>(rows * kp);
+        h->rf_BT = b.arr<double>(rows * kp);
+        h->rf_b = b.arr<double>(rows);
+        h->rf_w = b.arr<double>(rows);
+        h->rf_psi = b.arr<double>(rows);
+        h->rf_sd = b.arr<double>(rows);
+        h->rf_obj = b.arr<double>(h->rf_nparts);
+        h->rf_x = b.arr<double>(kp);
+        h->rf_g = b.arr<double>(kp);
+        h->rf_d = b.arr<double>(kp);
+        h->rf_r = b.arr<double>(kp);
+        h->rf_F = b.arr<double>(rup(kp, 8) * kp);
+        h->rf_H = b.arr<double>(kp * kp);
+        h->rf_ws = b.arr<double>((int64_t)factor_ws_doubles(kp));
+        GemvTDesc g{};
+        g.rows = rows; g.cols = kp;
+        int64_t need = 0;
+        plan_gemv_t(BICADMM_F64, &g, 1, h->sm_count, &need, 1);
+        h->rf_gt = g;
+        h->rf_part = b.arr<double>(need);
+    }
     h->cg_r = b.arr<double>(len);
     h->cg_p = b.arr<double>(len);
     h->cg_Ap = b.arr<double>(len);
@@ -718,6 +754,7 @@ int bicadmm_workspace_size(const bicadmm_problem* P, const bicadmm_params* R, si
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&tmp.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) tmp.sm_count = 148;
     tmp.C = P->C;
+    tmp.prm = *R;
     *bytes = plan(&tmp, P, nullptr);
     return BICADMM_OK;
 }
@@ -1428,6 +1465,105 @@ static int do_refit(bicadmm_handle* h) {
     return BICADMM_OK;
 }
 
+// Logistic refit on the support T (DESIGN R29), the oracle's algorithm on the GPU: damped
+// Newton from z on T with the exact k x k Hessian AT^T diag(s(1-s)) AT + lambda I (DMMA Gram
+// of the row-scaled gathered columns, blocked Cholesky inverse), Armijo backtracking on the
+// objective; the k-vectors' scalar logic (step size, stopping) runs on the host.
+static int do_refit_logistic(bicadmm_handle* h) {
+    const int64_t kp = h->rf_kp, rows = h->rf_rows, len = h->len;
+    const double lam = h->prm.lambda;
+    cudaStream_t st = h->st;
+    // gather the support columns of every local block and the labels
+    H_CUDA(h, cudaMemsetAsync(h->rf_AT, 0, sizeof(double) * rows * kp, st));
+    {
+        int64_t off = 0;
+        for (auto& nd : h->nod) {
+            for (auto& L : h->blk)
+                if (L.li == nd.li)
+                    H_RC(h, launch_rf_gather(h->dtype, L.A, L.lda, L.m, L.c0, L.nj, h->support, h->support_count,
+                                             h->rf_AT, kp, off, st));
+            H_RC(h, launch_to_f64(h->dtype, nd.m, nd.b, h->rf_b + off, st));
+            off += nd.m;
+        }
+    }
+    int64_t cnt = 0;
+    H_CUDA(h, cudaMemcpyAsync(&cnt, h->support_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    H_CUDA(h, cudaStreamSynchronize(st));
+    if (cnt <= 0) return BICADMM_OK;
+    // start: z on T (x_final holds z on the support here)
+    std::vector<int64_t> sup(cnt);
+    std::vector<double> zf(len), x(kp, 0.0), xn(kp, 0.0), g(kp), d(kp);
+    H_CUDA(h, cudaMemcpyAsync(sup.data(), h->support, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, st));
+    H_CUDA(h, cudaMemcpyAsync(zf.data(), h->x_final, sizeof(double) * len, cudaMemcpyDeviceToHost, st));
+    H_CUDA(h, cudaStreamSynchronize(st));
+    for (int64_t a = 0; a < cnt; ++a) x[a] = zf[sup[a]];
+    std::vector<double> parts(h->rf_nparts);
+    GemvDesc aw{h->rf_AT, kp, rows, kp, h->rf_x, h->rf_w, 0};
+    // f(v): uploads v into rf_x, leaves w = AT v in rf_w
+    auto objective = [&](const std::vector<double>& v, double& f) -> int {
+        H_CUDA(h, cudaMemcpyAsync(h->rf_x, v.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
+        H_RC(h, launch_gemv(BICADMM_F64, &aw, 1, h->gemv_cap, st, 1));
+        H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, nullptr, nullptr, h->rf_obj, st));
+        H_CUDA(h, cudaMemcpyAsync(parts.data(), h->rf_obj, sizeof(double) * parts.size(), cudaMemcpyDeviceToHost, st));
+        H_CUDA(h, cudaStreamSynchronize(st));
+        double s = 0.0, xx = 0.0;
+        for (double p : parts) s += p;
+        for (int64_t a = 0; a < kp; ++a) xx += v[a] * v[a];
+        f = s + 0.5 * lam * xx;
+        return BICADMM_OK;
+    };
+    double f = 0.0;
+    H_RC(h, objective(x, f));
+    const int64_t ldf = rup(kp, 8);
+    h->rf_newton = 0;
+    for (int it = 0; it < 100; ++it) {
+        // gradient AT^T psi + lambda x and Hessian AT^T diag(s(1-s)) AT + lambda I at x (w = AT x)
+        H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, h->rf_psi, h->rf_sd, h->rf_obj, st));
+        GemvTDesc gt = h->rf_gt;
+        gt.A = h->rf_AT; gt.lda = kp; gt.p = h->rf_psi; gt.delta = nullptr; gt.z = nullptr; gt.u = nullptr;
+        gt.r = h->rf_g; gt.partial = h->rf_part;
+        H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, 1));
+        H_RC(h, launch_rf_scale_rows(rows, kp, h->rf_AT, h->rf_sd, h->rf_BT, st));
+        H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+        // (padding columns >= |T| are zero in AT: their Hessian rows are lambda I, step 0)
+        int rc = factor_inverse(kp, h->rf_F, ldf, h->rf_H, kp, BICADMM_F64, h->rf_ws, st);
+        if (rc) return fail(h, rc, "logistic refit: Hessian not positive definite");
+        H_CUDA(h, cudaMemcpyAsync(g.data(), h->rf_g, sizeof(double) * kp, cudaMemcpyDeviceToHost, st));
+        H_CUDA(h, cudaStreamSynchronize(st));
+        for (int64_t a = 0; a < kp; ++a) g[a] += lam * x[a];
+        // d = -H^{-1} g
+        H_CUDA(h, cudaMemcpyAsync(h->rf_r, g.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
+        GemvDesc hd{h->rf_H, kp, kp, kp, h->rf_r, h->rf_d, 0};
+        hd.alpha = -1.0;
+        H_RC(h, launch_gemv(BICADMM_F64, &hd, 1, h->gemv_cap, st, 1));
+        H_CUDA(h, cudaMemcpyAsync(d.data(), h->rf_d, sizeof(double) * kp, cudaMemcpyDeviceToHost, st));
+        H_CUDA(h, cudaStreamSynchronize(st));
+        h->rf_newton = it + 1;
+        double gd = 0.0, dmax = 0.0, xmax = 1.0;
+        for (int64_t a = 0; a < cnt; ++a) {
+            gd += g[a] * d[a];
+            dmax = std::max(dmax, std::fabs(d[a]));
+            xmax = std::max(xmax, std::fabs(x[a]));
+        }
+        if (dmax <= 1e-13 * xmax) {
+            for (int64_t a = 0; a < cnt; ++a) x[a] += d[a];
+            break;
+        }
+        double alpha = 1.0, fn = f;
+        for (int ls = 0; ls < 60; ++ls, alpha *= 0.5) {
+            for (int64_t a = 0; a < kp; ++a) xn[a] = a < cnt ? x[a] + alpha * d[a] : 0.0;
+            H_RC(h, objective(xn, fn));
+            if (fn <= f + 1e-4 * alpha * gd) break;
+        }
+        x = xn;   // rf_w holds AT x for the accepted point
+        f = fn;
+    }
+    H_CUDA(h, cudaMemcpyAsync(h->rf_x, x.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
+    H_RC(h, launch_rf_scatter(kp, h->rf_x, h->support, h->support_count, h->x_final, st));
+    h->refit_iters = h->rf_newton;
+    return BICADMM_OK;
+}
+
 static int do_finalize(bicadmm_handle* h) {
     const int64_t len = h->len;
     H_RC(h, launch_support(len, h->prm.kappa, h->z, h->support, h->support_count, h->st));
@@ -1436,6 +1572,9 @@ static int do_finalize(bicadmm_handle* h) {
     k_scatter_support<<<(unsigned)((kk + 255) / 256), 256, 0, h->st>>>(h->z, h->support, h->support_count, h->x_final);
     BIC_LAUNCHED();
     if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
+    // logistic refit (DESIGN R29): single rank (the gathered support matrix is local)
+    if (h->prm.refit && h->loss == BICADMM_LOGISTIC && h->C == 1 && h->rf_AT && !(h->comm && h->comm->world > 1))
+        H_RC(h, do_refit_logistic(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
     for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0, L.xt});

@@ -129,6 +129,90 @@ int launch_axpy_scaled(int64_t n, double a, const double* x, double* y, cudaStre
 //   mode 0: o = a + b                       (q = p + delta;  zu = z - u uses mode 2)
 //   mode 1: o = a + b + c, d = a - o        (p = q + t1 + y0, diff = q - p)
 //   mode 2: o = a - b
+// ----------------------------------------------------------------------------- logistic refit
+// (DESIGN R29) on the support T, single rank: the support columns of every local row are
+// gathered into a dense FP64 matrix AT (rows of all local nodes stacked, kp columns).
+template <typename T>
+__global__ void k_rf_gather(const T* __restrict__ A, int64_t lda, int64_t m, int64_t c0, int64_t nj,
+                            const int64_t* __restrict__ sup, const int64_t* __restrict__ cnt, double* __restrict__ AT,
+                            int64_t kp, int64_t row_off) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * kp) return;
+    const int64_t r = e / kp, a = e % kp;
+    if (a >= *cnt) return;
+    const int64_t l = sup[a];
+    if (l < c0 || l >= c0 + nj) return;
+    AT[(row_off + r) * kp + a] = (double)A[r * lda + (l - c0)];
+}
+
+int launch_rf_gather(int dtype, const void* A, int64_t lda, int64_t m, int64_t c0, int64_t nj, const int64_t* sup,
+                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s) {
+    const int64_t n = m * kp;
+    if (n <= 0) return BICADMM_OK;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dtype == BICADMM_F64) k_rf_gather<double><<<g, 256, 0, s>>>(static_cast<const double*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off);
+    else k_rf_gather<float><<<g, 256, 0, s>>>(static_cast<const float*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// per row r: sp = sigma(b w); psi = -b (1 - sp) (the loss derivative); sd = sqrt(sp (1 - sp))
+// (root of the second derivative); objective partials ln(1 + exp(-b w)) per CTA (fixed order)
+constexpr int kRfThreads = 256;
+__global__ void __launch_bounds__(kRfThreads) k_rf_logit(int64_t n, const double* __restrict__ b,
+                                                         const double* __restrict__ w, double* __restrict__ psi,
+                                                         double* __restrict__ sd, double* __restrict__ objpart) {
+    __shared__ double scratch[32];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double f = 0.0;
+    if (r < n) {
+        const double y = -b[r] * w[r];
+        f = y > 0.0 ? y + log1p(exp(-y)) : log1p(exp(y));
+        if (psi) {
+            const double sp = 1.0 / (1.0 + exp(y));   // sigma(b w)
+            psi[r] = -b[r] * (1.0 - sp);
+            sd[r] = sqrt(sp * (1.0 - sp));
+        }
+    }
+    f = block_sum(f, scratch);
+    if (threadIdx.x == 0) objpart[blockIdx.x] = f;
+}
+
+int launch_rf_logit(int64_t n, const double* b, const double* w, double* psi, double* sd, double* objpart,
+                    cudaStream_t s) {
+    if (n <= 0) return BICADMM_OK;
+    k_rf_logit<<<(unsigned)((n + kRfThreads - 1) / kRfThreads), kRfThreads, 0, s>>>(n, b, w, psi, sd, objpart);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+int64_t rf_logit_parts(int64_t n) { return (n + kRfThreads - 1) / kRfThreads; }
+
+// BT = diag(sd) AT (row scaling), so BT^T BT = AT^T diag(sp (1 - sp)) AT
+__global__ void k_rf_scale_rows(int64_t n, int64_t kp, const double* __restrict__ AT, const double* __restrict__ sd,
+                                double* __restrict__ BT) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n * kp) BT[e] = sd[e / kp] * AT[e];
+}
+
+int launch_rf_scale_rows(int64_t n, int64_t kp, const double* AT, const double* sd, double* BT, cudaStream_t s) {
+    if (n * kp <= 0) return BICADMM_OK;
+    k_rf_scale_rows<<<(unsigned)((n * kp + 255) / 256), 256, 0, s>>>(n, kp, AT, sd, BT);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+__global__ void k_rf_scatter(const double* __restrict__ x, const int64_t* __restrict__ sup,
+                             const int64_t* __restrict__ cnt, double* __restrict__ xf) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < *cnt) xf[sup[a]] = x[a];
+}
+
+int launch_rf_scatter(int64_t kp, const double* x, const int64_t* sup, const int64_t* cnt, double* xf, cudaStream_t s) {
+    k_rf_scatter<<<(unsigned)((kp + 255) / 256), 256, 0, s>>>(x, sup, cnt, xf);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
 struct FatEwBatch { FatEw d[kMaxDesc]; int64_t begin[kMaxDesc + 1]; int nd; };
 
 __global__ void k_fat_ew(const FatEwBatch B, int mode) {

@@ -206,6 +206,14 @@ int launch_ridge_mask(int64_t n, const double* mask, const double* v, double lam
 int launch_cg_xr(int64_t n, const double* sc, const double* p, const double* Ap, double* x, double* r, cudaStream_t s);
 int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStream_t s);
 int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s);
+// logistic refit on the support (k_vec.cu; DESIGN R29)
+int launch_rf_gather(int dtype, const void* A, int64_t lda, int64_t m, int64_t c0, int64_t nj, const int64_t* sup,
+                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s);
+int launch_rf_logit(int64_t n, const double* b, const double* w, double* psi, double* sd, double* objpart,
+                    cudaStream_t s);
+int64_t rf_logit_parts(int64_t n);
+int launch_rf_scale_rows(int64_t n, int64_t kp, const double* AT, const double* sd, double* BT, cudaStream_t s);
+int launch_rf_scatter(int64_t kp, const double* x, const int64_t* sup, const int64_t* cnt, double* xf, cudaStream_t s);
 int launch_support_mask(int64_t cap, const int64_t* sup, const int64_t* cnt, double* mask, cudaStream_t s);
 struct FatEw { const double* a; const double* b; const double* c; double* o; double* d; int64_t n; };
 int launch_fat_ew(const FatEw* d, int nd, int mode, cudaStream_t s);   // k_vec.cu

@@ -363,3 +363,28 @@ def test_auto_sweep_choice(bc):
                        dg.block_partition(n, 1))
         assert s.sweep_kind() == (want, 0), (n, s.sweep_kind())
         s.close()
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 1e-4)], ids=["f64", "f32"])
+def test_logistic_refit_matches_oracle(bc, orc, dtype, tol):
+    # DESIGN R29: damped Newton refit on the support, GPU vs oracle (run to the same
+    # iterate, then the same refit; objective and x_final at the bar)
+    P = dg.generate(3, 500, 120, 8, "logistic", seed=12)
+    cs = dg.block_partition(120, 2)
+    prm = dict(kappa=8, max_outer=25, inner_fixed=5, refit=1, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], "logistic",
+                   bc.Params(**prm), cs)
+    s.iterate(25)
+    rep = s.finalize()
+    Aref = [a.to(dtype).double().numpy() for a in P.A]
+    bref = [b.to(dtype).double().numpy() for b in P.b]
+    ref = orc.run(orc.Problem(Aref, bref, orc.LOGISTIC, 1, np.array(cs)), orc.Params(**prm))
+    assert s.support().tolist() == ref["support"].tolist()
+    xf = s.get(bc.FIELD_X_FINAL)
+    assert _rel(xf, ref["x_final"]) <= tol
+    assert abs(rep.objective - ref["objective"]) <= tol * abs(ref["objective"])
+    # the refit lowers the objective relative to z on the support
+    z_on_T = np.zeros_like(xf)
+    T = ref["support"]
+    z_on_T[T] = ref["z"][T]
+    assert ref["objective"] <= orc.objective(orc.Problem(Aref, bref, orc.LOGISTIC, 1, np.array(cs)), 100.0, z_on_T)
