@@ -346,8 +346,13 @@ void plan_gemv_t(int dtype, GemvTDesc* d, int nd, int sm_count, int64_t* need, i
         d[k].nstrips = (int32_t)((d[k].cols + W - 1) / W);
         total_strips += d[k].nstrips;
     }
-    // ~24 CTA slots per SM over the launch (several waves at 3-4 resident CTAs/SM)
-    const int64_t target = (int64_t)sm_count * 24;
+    // C = 1: ~192 CTAs per SM over the launch, i.e. short row chunks, so that the CTAs in
+    // flight at any time touch a narrow band of rows (at 100 GB of A: 5.4 -> 6.2 TB/s, the
+    // wide-band variant thrashes address translation); C > 1: 24.  BICADMM_GEMVT_CTAS_PER_SM
+    // overrides (tuning)
+    static const int env_per_sm = [] { const char* e = getenv("BICADMM_GEMVT_CTAS_PER_SM"); return e && atoi(e) > 0 ? atoi(e) : 0; }();
+    const int per_sm = env_per_sm ? env_per_sm : (C > 1 ? 24 : 192);
+    const int64_t target = (int64_t)sm_count * per_sm;
     int64_t chunks = total_strips > 0 ? (target + total_strips - 1) / total_strips : 1;
     if (chunks < 1) chunks = 1;
     for (int k = 0; k < nd; ++k) {
