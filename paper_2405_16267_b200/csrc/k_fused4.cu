@@ -2,23 +2,23 @@
 //
 // Same algebra as the two-pass sweep (Eqs. (22)-(24)) for nodes with one local
 // block.  A cluster of 2 CTAs (2 SMs) owns a contiguous row range; CTA h of the pair
-// owns column half h of every row, so a 4-deep ring of half-rows fits in shared
-// memory even at n = 10^4 in FP64 (4 x 40 KB):
+// owns column half h of every row, so a 5-deep ring of half-rows fits in shared
+// memory even at n = 10^4 in FP64 (5 x 40 KB):
 //
-//   producer warp : TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of half-row
-//                   k + 2 into the ring while rows k, k+1 are being used
-//   12 main warps : dot of half-row k with x (x half in registers) -> 12 partials
-//                   written to BOTH CTAs' smem (local st.shared + DSMEM st.shared::cluster)
-//                   with release arrives on both CTAs' "dot" mbarriers;
-//                   axpy acc[col] += A[k-2, col] q_{k-2} from the ring (no second read)
+//   producer warp : TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of a half-row
+//                   into the ring as soon as its slot is released
+//   12 main warps : dot of half-row k with x (x half in registers) -> 12 partials,
+//                   kept locally and sent to the peer CTA with st.async (mbarrier
+//                   complete_tx on the peer's "dot" barrier: no cluster-scope fence);
+//                   axpy acc[col] += A[k-D, col] q_{k-D} from the ring (no second read)
 //   3 prox warps  : wait for the 24 partials of a row, p = fixed-order sum (identical
 //                   in both CTAs), omega = prox(p + nu) (22), nu += p - omega (23),
 //                   delta = omega - p - nu, q = p + delta; rank 0 stores p, nu, delta.
 //
 // Both CTAs compute the prox redundantly from bit-identical inputs, so the only
-// cluster traffic per row is 12 doubles + one remote arrive each way.  A crosses
-// HBM exactly once per sweep; partial products are written per cluster and reduced
-// in fixed order by the next sweep's Eq. (24) epilogue (bit-reproducible).
+// cluster traffic per row is 12 doubles each way.  A crosses HBM exactly once per
+// sweep; partial products are written per (cluster, row group) and reduced in fixed
+// order by the next sweep's Eq. (24) epilogue (bit-reproducible).
 #include <cfloat>
 #include <stdlib.h>
 
@@ -33,7 +33,6 @@ constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp 
 constexpr int kF4MainT = 32 * kF4Main;         // 384
 constexpr int kF4RingMax = 16;                 // half-row ring depth (runtime nring <= 16, by smem)
 constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
-constexpr int kF4DL2 = 8;                      // axpy delay when the axpy re-reads the row from L2
 constexpr int kF4Q = 32;                       // dot / q slots (>= delay + lag window)
 
 __device__ __forceinline__ double f4_sigmoid(double a) {
@@ -138,17 +137,14 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// MODE 0: the axpy of row k - 2 reads the smem ring (slot held until then);
-// MODE 1: the axpy re-reads half-row k - kF4DL2 from L2 (slot released after the dot);
-// MODE 2: each thread keeps its own columns of rows k-1, k-2 in registers (a delay
-//         line), x lives in smem, and the slot is released right after the dot -> the
-//         ring keeps nring - 1 half-rows in flight.
-template <typename T, int E, int MODE, int GR>
+// The axpy of row k - D reads the row from its smem ring slot, held until then (measured
+// alternatives -- an L2 re-read for the axpy, a register delay line -- were slower and are
+// described in DESIGN.md section 6).
+template <typename T, int E, int GR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
     k_fused4(const Fused2Args a, int loss, double rho, int nring, int dly, int ngrp) {
-    constexpr bool L2AX = MODE == 1;
-    const int D = L2AX ? kF4DL2 : dly;   // axpy delay (rows; in a group's own rows when ngrp > 1)
-    // row groups (MODE 0): the 12 main warps form ngrp groups of W warps; group gi owns the
+    const int D = dly;   // axpy delay (rows; in a group's own rows when ngrp > 1)
+    // row groups: the 12 main warps form ngrp groups of W warps; group gi owns the
     // rows rb + gi, rb + gi + ngrp, ...  For narrow rows this overlaps the per-row latency
     // chain of ngrp rows.  Every row's dot has W partials per CTA.
     if (GR == 1) ngrp = 1;               // GR = 1: one group, W = 12 at compile time
@@ -215,90 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                                  &bar_full[s]);
             }
         }
-    } else if (MODE == 2 && warp < kF4Main) {
-        // ------------------------------------------------------------ main warps, register delay line
-        const int mt = threadIdx.x;
-        const unsigned peer = h ^ 1u;
-        double* xs = reinterpret_cast<double*>(f4_smem + (size_t)nring * half_pad * sizeof(T));
-        int ndd = nd0, nda = nd0;
-        double acc[E], h0[E], h1[E];
-        int64_t hc0, hcn, ac0, acn;
-        auto load_x = [&](int nd) {   // main warps only (named barrier 1)
-            half_range(nd, hc0, hcn);
-            asm volatile("bar.sync 1, %0;" ::"n"(kF4MainT));
-            for (int64_t c = mt; c < hcn; c += kF4MainT) xs[c] = a.x[nd][hc0 + c];
-            asm volatile("bar.sync 1, %0;" ::"n"(kF4MainT));
-        };
-        load_x(ndd);
-        half_range(nda, ac0, acn);
-#pragma unroll
-        for (int e = 0; e < E; ++e) { acc[e] = 0.0; h0[e] = 0.0; h1[e] = 0.0; }
-        auto flush = [&](int node) {
-            double* out = a.partial[node] + (clu - a.cta_lo[node]) * a.ncols[node] + ac0;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int64_t c = mt + (int64_t)kF4MainT * e;
-                if (c < acn) out[c] = acc[e];
-                acc[e] = 0.0;
-            }
-        };
-        RingPos pd;
-        auto step = [&](int64_t k, double (&H)[E]) {
-            double tmp[E];
-            if (k < re) {
-                const int nn2 = node_of(k, ndd);
-                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
-                const int s = pd.s;
-                mb4_wait_cta(&bar_full[s], pd.ph);
-                pd.next(nring);
-                const T* row = ring + s * half_pad;
-                double dot = 0.0;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int64_t c = mt + (int64_t)kF4MainT * e;
-                    tmp[e] = c < hcn ? (double)row[c] : 0.0;
-                    if (c < hcn) dot = fma(tmp[e], xs[c], dot);
-                }
-                __syncwarp();
-                if (lane == 0) mb4_arrive_local(&bar_empty[s]);   // slot free: row k now in registers
-                if (!a.active[ndd]) dot = 0.0;
-                dot = warp_sum(dot);
-                if (lane == 0) {
-                    const int q = (int)((k - rb) % kF4Q);
-                    const int idx = (int)h * kF4Main + warp;
-                    dotp[q][idx] = dot;
-                    st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
-                    if (warp == 0) mb4_expect_tx(&bar_dot[q], 8u * kF4Main);   // the peer's 12 stores
-                    else mb4_arrive_local(&bar_dot[q]);
-                }
-            }
-            const int64_t ra = k - 2;   // its columns are in H
-            if (ra >= rb && ra < re) {
-                const int nn2 = node_of(ra, nda);
-                if (nn2 != nda) {
-                    if (a.active[nda]) flush(nda);
-                    nda = nn2;
-                    half_range(nda, ac0, acn);
-                }
-                const int q = (int)((ra - rb) % kF4Q);
-                mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
-                const double qq = qv[q];
-                if (a.active[nda]) {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) acc[e] = fma(H[e], qq, acc[e]);
-                }
-            }
-            if (k < re) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) H[e] = tmp[e];
-            }
-        };
-        for (int64_t k = rb; k < re + 2; k += 2) {
-            step(k, h0);
-            step(k + 1, h1);
-        }
-        if (a.active[nda]) flush(nda);
-    } else if (MODE == 0 && GR == 0 && warp < kF4Main) {
+    } else if (GR == 0 && warp < kF4Main) {
         // ------------------------------------------------------------ main warps (row groups)
         const int gi = warp / W, wig = warp % W;
         const int GT = 32 * W;                 // threads of a group (cover a half-row)
@@ -384,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             }
         }
         if (a.active[nda]) flush(nda);
-    } else if ((MODE == 1 || GR == 1) && warp < kF4Main) {
+    } else if (GR == 1 && warp < kF4Main) {
         // ------------------------------------------------------------ main warps (one group)
         const int mt = threadIdx.x;
         const unsigned peer = h ^ 1u;
@@ -430,10 +343,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                         if (c < hcn) dot = fma((double)row[c], xr[e], dot);
                     }
                 }
-                if constexpr (L2AX) {   // ring slot free as soon as every warp has read it
-                    __syncwarp();
-                    if (lane == 0) mb4_arrive_local(&bar_empty[s]);
-                }
                 dot = warp_sum(dot);
                 if (lane == 0) {
                     const int q = (int)((k - rb) % kF4Q);
@@ -454,20 +363,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                 }
                 const int q = (int)((ra - rb) % kF4Q);
                 const bool on = a.active[nda];
-                if constexpr (L2AX) {
-                    // issue the L2 re-read of half-row ra before waiting for its q
-                    const T* grow = static_cast<const T*>(a.A[nda]) + (ra - a.row_off[nda]) * a.lda[nda] + ac0;
-                    double v[E];
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const int64_t c = mt + (int64_t)kF4MainT * e;
-                        v[e] = (on && c < acn) ? (double)__ldg(grow + c) : 0.0;
-                    }
-                    mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
-                    const double qq = qv[q];
-#pragma unroll
-                    for (int e = 0; e < E; ++e) acc[e] = fma(v[e], qq, acc[e]);
-                } else {
                     mb4_wait_cta(&bar_q[q], (unsigned)(((ra - rb) / kF4Q) & 1));
                     const double qq = qv[q];
                     const int s = pa.s;
@@ -482,7 +377,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                     }
                     __syncwarp();
                     if (lane == 0) mb4_arrive_local(&bar_empty[s]);
-                }
             }
         }
         if (a.active[nda]) flush(nda);
@@ -530,14 +424,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
 int fused4_max_cols(int dtype) { return dtype == BICADMM_F64 ? 2 * kF4MainT * 16 : 2 * kF4MainT * 16; }
 
 static size_t f4_slot_bytes(const Fused2Args& a, size_t es) { return (size_t)(((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * es; }
-static int f4_mode() {
-    static int m = [] { const char* e = getenv("BICADMM_F4_MODE"); int v = e ? atoi(e) : 0; return v >= 0 && v <= 2 ? v : 0; }();
-    return m;
-}
-static size_t f4_xs_bytes(const Fused2Args& a) { return f4_mode() == 2 ? f4_slot_bytes(a, 8) : 0; }
 static int f4_ring(const Fused2Args& a, size_t es) {
     const char* e = getenv("BICADMM_F4_RING");
-    int r = (int)((210 * 1024 - f4_xs_bytes(a)) / f4_slot_bytes(a, es));
+    int r = (int)((210 * 1024) / f4_slot_bytes(a, es));
     if (e) r = atoi(e) < r ? atoi(e) : r;
     return r > kF4RingMax ? kF4RingMax : r;
 }
@@ -548,7 +437,6 @@ static int f4_ring(const Fused2Args& a, size_t es) {
 // 3 groups (E = 16) 2.86 ms per sweep.
 int fused4_groups(int dtype, int64_t max_cols) {
     (void)dtype;
-    if (f4_mode() != 0) return 1;
     const int64_t half = (max_cols + 1) / 2 + 2;
     int g = 1;
     const int cand[4] = {6, 4, 3, 2};
@@ -572,21 +460,21 @@ static int f4_delay(int nring, int ngrp) {
     return v;
 }
 
-template <typename T, int MODE, int GR>
+template <typename T, int GR>
 static int f4_launch(int E, int ngrp, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
     const int nring = f4_ring(a, sizeof(T));
     if (nring < 4 || ngrp >= nring - 1) return BICADMM_ERR_INVALID;
-    const size_t smem = (size_t)nring * f4_slot_bytes(a, sizeof(T)) + f4_xs_bytes(a);
+    const size_t smem = (size_t)nring * f4_slot_bytes(a, sizeof(T));
 #define F4_CASE(EE)                                                                                            \
     case EE: {                                                                                                 \
         static bool set = false;                                                                               \
         if (!set) {                                                                                            \
-            if (cudaFuncSetAttribute(k_fused4<T, EE, MODE, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+            if (cudaFuncSetAttribute(k_fused4<T, EE, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                      212 * 1024) != cudaSuccess)                                               \
                 return BICADMM_ERR_CUDA;                                                                       \
             set = true;                                                                                        \
         }                                                                                                      \
-        k_fused4<T, EE, MODE, GR><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring, f4_delay(nring, ngrp), ngrp); \
+        k_fused4<T, EE, GR><<<grid, kF4Threads, smem, s>>>(a, loss, rho, nring, f4_delay(nring, ngrp), ngrp); \
         break;                                                                                                 \
     }
     switch (E) {
@@ -610,19 +498,11 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     // and are whole 16-byte multiples
     const int64_t es = dtype == BICADMM_F64 ? 8 : 4;
     for (int k = 0; k < a.nn; ++k) if ((a.ncols[k] * es) % 16 || (a.lda[k] * es) % 16) return BICADMM_ERR_INVALID;
-    // BICADMM_F4_MODE: 0 (default) ring-held rows, 1 L2 re-read, 2 register delay line
-    const int mode = f4_mode();
     int rc;
     if (dtype == BICADMM_F64)
-        rc = mode == 2 ? f4_launch<double, 2, 1>(E, 1, a, loss, rho, grid, s)
-           : mode == 1 ? f4_launch<double, 1, 1>(E, 1, a, loss, rho, grid, s)
-           : ngrp == 1 ? f4_launch<double, 0, 1>(E, 1, a, loss, rho, grid, s)
-                       : f4_launch<double, 0, 0>(E, ngrp, a, loss, rho, grid, s);
+        rc = ngrp == 1 ? f4_launch<double, 1>(E, 1, a, loss, rho, grid, s) : f4_launch<double, 0>(E, ngrp, a, loss, rho, grid, s);
     else
-        rc = mode == 2 ? f4_launch<float, 2, 1>(E, 1, a, loss, rho, grid, s)
-           : mode == 1 ? f4_launch<float, 1, 1>(E, 1, a, loss, rho, grid, s)
-           : ngrp == 1 ? f4_launch<float, 0, 1>(E, 1, a, loss, rho, grid, s)
-                       : f4_launch<float, 0, 0>(E, ngrp, a, loss, rho, grid, s);
+        rc = ngrp == 1 ? f4_launch<float, 1>(E, 1, a, loss, rho, grid, s) : f4_launch<float, 0>(E, ngrp, a, loss, rho, grid, s);
     if (rc) return rc;
     BIC_LAUNCHED();
     return BICADMM_OK;
