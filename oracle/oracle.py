@@ -96,6 +96,7 @@ def lib() -> ct.CDLL:
         L.orc_ridge_dense.argtypes = [ct.POINTER(_Problem), _f64, _pd]
         L.orc_refit_ls.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pd]
         L.orc_refit_logistic.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pd]
+        L.orc_refit_softmax.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pd]
         L.orc_best_subset.argtypes = [ct.POINTER(_Problem), _f64, _i64, _pi64, _pi64, _pd, _pd]
         _lib = L
     return _lib
@@ -353,6 +354,15 @@ def refit_logistic(problem: Problem, gamma: float, T, x0) -> np.ndarray:
     x = np.ascontiguousarray(x0, dtype=np.float64).copy()
     ps = problem.struct()
     _rc(lib().orc_refit_logistic(ct.byref(ps), gamma, T.size, T.ctypes.data_as(_pi64), _d(x)))
+    return x
+
+
+def refit_softmax(problem: Problem, gamma: float, T, x0) -> np.ndarray:
+    """Softmax refit on the entry support T of vec(X) (DESIGN R29), damped Newton from x0."""
+    T = np.ascontiguousarray(T, dtype=np.int64)
+    x = np.ascontiguousarray(x0, dtype=np.float64).copy()
+    ps = problem.struct()
+    _rc(lib().orc_refit_softmax(ct.byref(ps), gamma, T.size, T.ctypes.data_as(_pi64), _d(x)))
     return x
 
 

@@ -676,10 +676,11 @@ int orc_run(const orc_problem* pb, const orc_params* pr, const int32_t* schedule
             rc = orc_refit_ls(pb, pr->gamma, T, sup, xt);
             for (int64_t a = 0; a < T; ++a) res->x_final[sup[a]] = xt[a];
             free(xt);
-        } else if (pr->refit && pb->loss == ORC_LOGISTIC && T > 0) {
+        } else if (pr->refit && (pb->loss == ORC_LOGISTIC || pb->loss == ORC_SOFTMAX) && T > 0) {
             double* xt = (double*)malloc(sizeof(double) * (size_t)T);
             for (int64_t a = 0; a < T; ++a) xt[a] = z[sup[a]];   /* start at z on T */
-            rc = orc_refit_logistic(pb, pr->gamma, T, sup, xt);
+            rc = pb->loss == ORC_LOGISTIC ? orc_refit_logistic(pb, pr->gamma, T, sup, xt)
+                                          : orc_refit_softmax(pb, pr->gamma, T, sup, xt);
             for (int64_t a = 0; a < T; ++a) res->x_final[sup[a]] = xt[a];
             free(xt);
         } else {
@@ -785,7 +786,8 @@ int orc_refit_ls(const orc_problem* pb, double gamma, int64_t k, const int64_t* 
 /* Logistic refit on support T (DESIGN R29): minimise the objective (1) restricted to T,
  *   f(x_T) = sum_i sum_r ln(1 + exp(-b_r (A_iT x_T)_r)) + ||x_T||^2 / (2 gamma),
  * by Newton's method with the exact k x k Hessian sum_i A_iT^T diag(s(1-s)) A_iT + I/gamma
- * (s = sigma(b w)), Cholesky solves, and Armijo backtracking on f (factor 1/2, c = 1e-4).
+ * (s = sigma(b w)), Cholesky solves, and Armijo backtracking on f (factor 1/2, c = 1e-4) while
+ * the predicted decrease -g'd exceeds 1e-12 (1 + |f|) (below that f cannot resolve it).
  * x holds the start on entry (z on T) and the minimiser on exit; stops when the Newton
  * step's max-norm is <= 1e-13 max(1, ||x||_inf) (at most 100 steps). */
 static double logistic_refit_f(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, const double* x) {
@@ -843,16 +845,110 @@ int orc_refit_logistic(const orc_problem* pb, double gamma, int64_t k, const int
             for (int64_t a = 0; a < k; ++a) x[a] += d[a];
             break;
         }
+        /* Armijo backtracking; once the predicted decrease -g'd is below the objective's
+         * resolution the full (locally quadratically convergent) Newton step is taken */
+        const int resolve = -gd > 1e-12 * (1.0 + fabs(f));
         double alpha = 1.0, fn = f;
         for (int ls = 0; ls < 60; ++ls, alpha *= 0.5) {
             for (int64_t a = 0; a < k; ++a) xn[a] = x[a] + alpha * d[a];
             fn = logistic_refit_f(pb, gamma, k, T, xn);
-            if (fn <= f + 1e-4 * alpha * gd) break;
+            if (!resolve || fn <= f + 1e-4 * alpha * gd) break;
         }
         memcpy(x, xn, sizeof(double) * (size_t)k);
         f = fn;
     }
     free(F); free(g); free(d); free(xn);
+    return rc;
+}
+
+/* Softmax refit on the entry support T of vec(X) (X in R^{n x C}, entry a = l*C + c;
+ * DESIGN R13, R29): the same damped Newton as the logistic refit on
+ *   f(x_T) = sum_i sum_r [logsumexp(w_r) - w_{r, y_r}] + ||x_T||^2 / (2 gamma),
+ *   w_r[c] = sum_{a in T, c_a = c} A[r][l_a] x_a,
+ * gradient g_a = sum_r A[r][l_a] (p_r[c_a] - [y_r = c_a]) + x_a / gamma and exact Hessian
+ * H_ab = sum_r A[r][l_a] A[r][l_b] (p_r[c_a] [c_a = c_b] - p_r[c_a] p_r[c_b]) + [a = b] / gamma. */
+static void softmax_row(int C, const double* w, double* p) {
+    double mx = w[0];
+    for (int c = 1; c < C; ++c) if (w[c] > mx) mx = w[c];
+    double se = 0.0;
+    for (int c = 0; c < C; ++c) { p[c] = exp(w[c] - mx); se += p[c]; }
+    for (int c = 0; c < C; ++c) p[c] /= se;
+}
+
+static double softmax_refit_f(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, const double* x,
+                              double* w) {
+    const int C = pb->C;
+    double f = 0.0;
+    for (int i = 0; i < pb->N; ++i)
+        for (int64_t r = 0; r < pb->m[i]; ++r) {
+            for (int c = 0; c < C; ++c) w[c] = 0.0;
+            for (int64_t a = 0; a < k; ++a) w[T[a] % C] += pb->A[i][r * pb->n + T[a] / C] * x[a];
+            f += orc_phi(ORC_SOFTMAX, C, w, pb->b[i][r]);
+        }
+    double xx = 0.0;
+    for (int64_t a = 0; a < k; ++a) xx += x[a] * x[a];
+    return f + xx / (2.0 * gamma);
+}
+
+int orc_refit_softmax(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x) {
+    if (pb->loss != ORC_SOFTMAX || pb->C < 2) return ORC_ERR_INVALID;
+    const int C = pb->C;
+    double* F = (double*)malloc(sizeof(double) * (size_t)(k * k + 1));
+    double* g = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double* d = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double* xn = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double* a_r = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+    double w[64], p[64];
+    int rc = ORC_OK;
+    double f = softmax_refit_f(pb, gamma, k, T, x, w);
+    for (int it = 0; it < 100 && rc == ORC_OK; ++it) {
+        for (int64_t a = 0; a < k; ++a) g[a] = x[a] / gamma;
+        for (int64_t a = 0; a < k * k; ++a) F[a] = 0.0;
+        for (int64_t a = 0; a < k; ++a) F[a * k + a] = 1.0 / gamma;
+        for (int i = 0; i < pb->N; ++i)
+            for (int64_t r = 0; r < pb->m[i]; ++r) {
+                for (int c = 0; c < C; ++c) w[c] = 0.0;
+                for (int64_t a = 0; a < k; ++a) {
+                    a_r[a] = pb->A[i][r * pb->n + T[a] / C];
+                    w[T[a] % C] += a_r[a] * x[a];
+                }
+                softmax_row(C, w, p);
+                const int y = (int)pb->b[i][r];
+                for (int64_t a = 0; a < k; ++a) {
+                    const int ca = (int)(T[a] % C);
+                    g[a] += a_r[a] * (p[ca] - (ca == y ? 1.0 : 0.0));
+                    for (int64_t bb = 0; bb <= a; ++bb) {
+                        const int cb = (int)(T[bb] % C);
+                        F[a * k + bb] += a_r[a] * a_r[bb] * (p[ca] * (ca == cb ? 1.0 : 0.0) - p[ca] * p[cb]);
+                    }
+                }
+            }
+        for (int64_t a = 0; a < k; ++a)
+            for (int64_t c = 0; c < a; ++c) F[c * k + a] = F[a * k + c];
+        for (int64_t a = 0; a < k; ++a) d[a] = -g[a];
+        rc = spd_solve(k, F, d);
+        if (rc != ORC_OK) break;
+        double gd = 0.0, dmax = 0.0, xmax = 1.0;
+        for (int64_t a = 0; a < k; ++a) {
+            gd += g[a] * d[a];
+            dmax = fmax(dmax, fabs(d[a]));
+            xmax = fmax(xmax, fabs(x[a]));
+        }
+        if (dmax <= 1e-13 * xmax) {
+            for (int64_t a = 0; a < k; ++a) x[a] += d[a];
+            break;
+        }
+        const int resolve = -gd > 1e-12 * (1.0 + fabs(f));   /* as in the logistic refit */
+        double alpha = 1.0, fn = f;
+        for (int ls = 0; ls < 60; ++ls, alpha *= 0.5) {
+            for (int64_t a = 0; a < k; ++a) xn[a] = x[a] + alpha * d[a];
+            fn = softmax_refit_f(pb, gamma, k, T, xn, w);
+            if (!resolve || fn <= f + 1e-4 * alpha * gd) break;
+        }
+        memcpy(x, xn, sizeof(double) * (size_t)k);
+        f = fn;
+    }
+    free(F); free(g); free(d); free(xn); free(a_r);
     return rc;
 }
 

@@ -104,6 +104,8 @@ int orc_ridge_dense(const orc_problem* pb, double gamma, double* x);
 int orc_refit_ls(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x);
 /* Logistic refit on T by damped Newton (DESIGN R29); x: start (z on T) in, minimiser out. */
 int orc_refit_logistic(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x);
+/* Softmax refit on the entry support T of vec(X) (DESIGN R29), same damped Newton. */
+int orc_refit_softmax(const orc_problem* pb, double gamma, int64_t k, const int64_t* T, double* x);
 int orc_best_subset(const orc_problem* pb, double gamma, int64_t kappa,
                     int64_t* support, int64_t* support_len, double* x, double* objective);
 

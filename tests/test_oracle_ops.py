@@ -474,3 +474,58 @@ def test_run_logistic_refit_is_refit_of_z(orc):
     x = orc.refit_logistic(pb, 100.0, T, r["z"][T])
     assert np.allclose(r["x_final"][T], x, rtol=0, atol=1e-12)
     assert np.count_nonzero(r["x_final"]) <= 3
+
+
+@pytest.mark.parametrize("gamma", [100.0, 0.5])
+def test_refit_softmax_matches_scipy(orc, gamma):
+    # DESIGN R29 for softmax: entry support of vec(X), pinned against scipy BFGS on the
+    # objective written with numpy (logsumexp - w_y) and against KKT
+    rng = np.random.default_rng(9)
+    C, n, m = 4, 10, 90
+    A = [rng.normal(size=(m, n)) / np.sqrt(m) for _ in range(2)]
+    Xt = np.zeros((n, C))
+    Xt[2, 1], Xt[5, 3], Xt[7, 0] = 2.0, -1.5, 1.0
+    y = [np.argmax(a @ Xt + 0.3 * rng.normal(size=(m, C)), axis=1).astype(float) for a in A]
+    T = np.array([2 * C + 1, 5 * C + 3, 7 * C + 0, 7 * C + 2, 9 * C + 1])
+    L, Cc = T // C, T % C
+    pb = orc.Problem(A, y, orc.SOFTMAX, C, np.array([0, n]))
+
+    def W(a, x):
+        w = np.zeros((a.shape[0], C))
+        for k in range(T.size):
+            w[:, Cc[k]] += a[:, L[k]] * x[k]
+        return w
+
+    def f(x):
+        s = 0.0
+        for a, yy in zip(A, y):
+            w = W(a, x)
+            s += (np.logaddexp.reduce(w, axis=1) - w[np.arange(len(yy)), yy.astype(int)]).sum()
+        return s + x @ x / (2 * gamma)
+
+    def g(x):
+        out = x / gamma
+        for a, yy in zip(A, y):
+            w = W(a, x)
+            p = np.exp(w - w.max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            p[np.arange(len(yy)), yy.astype(int)] -= 1.0
+            out = out + np.array([a[:, L[k]] @ p[:, Cc[k]] for k in range(T.size)])
+        return out
+
+    ref = optimize.minimize(f, np.zeros(T.size), jac=g, method="BFGS", options={"gtol": 1e-13, "maxiter": 10000})
+    x = orc.refit_softmax(pb, gamma, T, np.zeros(T.size))
+    assert np.max(np.abs(g(x))) <= 1e-11
+    assert np.max(np.abs(x - ref.x)) <= 1e-7 * max(1.0, np.max(np.abs(ref.x)))
+
+
+def test_run_softmax_refit_is_refit_of_z(orc):
+    rng = np.random.default_rng(11)
+    C, n, m = 3, 12, 70
+    A = [rng.normal(size=(m, n)) / np.sqrt(m) for _ in range(2)]
+    y = [rng.integers(0, C, size=m).astype(float) for _ in range(2)]
+    pb = orc.Problem(A, y, orc.SOFTMAX, C, np.array([0, n]))
+    r = orc.run(pb, orc.Params(kappa=4, max_outer=40, inner_fixed=4, refit=1))
+    T = r["support"]
+    x = orc.refit_softmax(pb, 100.0, T, r["z"][T])
+    assert np.allclose(r["x_final"][T], x, rtol=0, atol=1e-12)
