@@ -110,7 +110,7 @@ typedef struct {
     double eps_inner;     /* tol mode: stop node i when ||abar-obar|| <= eps_inner sqrt(m_i C)
                              and ||x_i^new - x_i^old|| <= eps_inner */
     int32_t max_inner;    /* tol mode cap */
-    int32_t refit;        /* refit on the final support: LS closed-form ridge (DESIGN R19), logistic
+    int32_t refit;        /* refit on the final support: LS closed-form ridge (DESIGN R19), logistic and softmax
                              damped Newton (DESIGN R29, single rank); softmax / hinge: x_final = z on T */
     int32_t sweep;        /* inner-sweep schedule: 0 = auto (the fastest measured: currently two-pass),
                              1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),

@@ -167,7 +167,9 @@ struct bicadmm_handle {
     int64_t rf_kp = 0, rf_rows = 0, rf_nparts = 0;
     double *rf_AT = nullptr, *rf_BT = nullptr, *rf_b = nullptr, *rf_w = nullptr, *rf_psi = nullptr,
            *rf_sd = nullptr, *rf_obj = nullptr, *rf_x = nullptr, *rf_g = nullptr, *rf_d = nullptr,
-           *rf_F = nullptr, *rf_H = nullptr, *rf_ws = nullptr, *rf_part = nullptr, *rf_r = nullptr;
+           *rf_F = nullptr, *rf_H = nullptr, *rf_ws = nullptr, *rf_part = nullptr, *rf_r = nullptr,
+           *rf_U = nullptr, *rf_W = nullptr, *rf_G = nullptr, *rf_P = nullptr, *rf_F2 = nullptr, *rf_X = nullptr,
+           *rf_Y = nullptr, *rf_xt = nullptr;   // softmax (C classes)
     GemvTDesc rf_gt{};
     int rf_newton = 0;
     int64_t gram_stride = 0, fws_stride = 0; // per-job setup scratch (doubles)
@@ -430,7 +432,7 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     // setup scratch: FP64 Gram / factor workspace
     const int64_t ldg = rup(kdmax, 8);
     h->mask = b.arr<double>(len);
-    if (P->loss == BICADMM_LOGISTIC && C == 1 && h->prm.refit) {
+    if (((P->loss == BICADMM_LOGISTIC && C == 1) || P->loss == BICADMM_SOFTMAX) && h->prm.refit) {
         int64_t rows = 0;
         for (auto& nd : h->nod) rows += nd.m;
         const int64_t kk = std::max<int64_t>(1, std::min<int64_t>(h->prm.kappa, len));
@@ -455,9 +457,19 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         GemvTDesc g{};
         g.rows = rows; g.cols = kp;
         int64_t need = 0;
-        plan_gemv_t(BICADMM_F64, &g, 1, h->sm_count, &need, 1);
+        plan_gemv_t(BICADMM_F64, &g, 1, h->sm_count, &need, C);
         h->rf_gt = g;
         h->rf_part = b.arr<double>(need);
+        if (C > 1) {
+            h->rf_U = b.arr<double>(rows * kp);
+            h->rf_W = b.arr<double>(rows * C);
+            h->rf_G = b.arr<double>(rows * C);
+            h->rf_P = b.arr<double>(rows * C);
+            h->rf_F2 = b.arr<double>(rup(kp, 8) * kp);
+            h->rf_X = b.arr<double>(kp * C);
+            h->rf_Y = b.arr<double>(kp * C);
+            h->rf_xt = b.arr<double>(kp * C);
+        }
     }
     h->cg_r = b.arr<double>(len);
     h->cg_p = b.arr<double>(len);
@@ -1465,15 +1477,20 @@ static int do_refit(bicadmm_handle* h) {
     return BICADMM_OK;
 }
 
-// Logistic refit on the support T (DESIGN R29), the oracle's algorithm on the GPU: damped
-// Newton from z on T with the exact k x k Hessian AT^T diag(s(1-s)) AT + lambda I (DMMA Gram
-// of the row-scaled gathered columns, blocked Cholesky inverse), Armijo backtracking on the
-// objective; the k-vectors' scalar logic (step size, stopping) runs on the host.
-static int do_refit_logistic(bicadmm_handle* h) {
+// Logistic / softmax refit on the support T (DESIGN R29), the oracle's algorithm on the GPU:
+// damped Newton from z on T with the exact k x k Hessian, Armijo backtracking on the objective
+// while it can resolve the predicted decrease; the support columns of every local row are
+// gathered once into AT (rows x kp, FP64).  Logistic: w = AT x, Hessian = Gram of the
+// row-scaled AT (sqrt(s(1-s))) + lambda I.  Softmax (entries a = l*C + c, c_a = a % C):
+// W = AT X with X[a][c] = x_a [c = c_a] (DMMA multi-class GEMV), gradient weights P - E_y,
+// Hessian = [c_a = c_b] Gram(sqrt(P_{c_a}) AT) - Gram(P_{c_a} AT) + lambda I.  The k-vectors'
+// scalar logic (step, stopping) runs on the host.
+static int do_refit_newton(bicadmm_handle* h) {
     const int64_t kp = h->rf_kp, rows = h->rf_rows, len = h->len;
+    const int C = h->C;
+    const bool sm = h->loss == BICADMM_SOFTMAX;
     const double lam = h->prm.lambda;
     cudaStream_t st = h->st;
-    // gather the support columns of every local block and the labels
     H_CUDA(h, cudaMemsetAsync(h->rf_AT, 0, sizeof(double) * rows * kp, st));
     {
         int64_t off = 0;
@@ -1481,7 +1498,7 @@ static int do_refit_logistic(bicadmm_handle* h) {
             for (auto& L : h->blk)
                 if (L.li == nd.li)
                     H_RC(h, launch_rf_gather(h->dtype, L.A, L.lda, L.m, L.c0, L.nj, h->support, h->support_count,
-                                             h->rf_AT, kp, off, st));
+                                             h->rf_AT, kp, off, st, C));
             H_RC(h, launch_to_f64(h->dtype, nd.m, nd.b, h->rf_b + off, st));
             off += nd.m;
         }
@@ -1490,26 +1507,34 @@ static int do_refit_logistic(bicadmm_handle* h) {
     H_CUDA(h, cudaMemcpyAsync(&cnt, h->support_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     H_CUDA(h, cudaStreamSynchronize(st));
     if (cnt <= 0) return BICADMM_OK;
-    // start: z on T (x_final holds z on the support here)
     std::vector<int64_t> sup(cnt);
-    std::vector<double> zf(len), x(kp, 0.0), xn(kp, 0.0), g(kp), d(kp);
+    std::vector<double> zf(len), x(kp, 0.0), xn(kp, 0.0), g(kp), d(kp), Xh(sm ? kp * C : 0), Yh(sm ? kp * C : 0);
     H_CUDA(h, cudaMemcpyAsync(sup.data(), h->support, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost, st));
     H_CUDA(h, cudaMemcpyAsync(zf.data(), h->x_final, sizeof(double) * len, cudaMemcpyDeviceToHost, st));
     H_CUDA(h, cudaStreamSynchronize(st));
-    for (int64_t a = 0; a < cnt; ++a) x[a] = zf[sup[a]];
+    for (int64_t a = 0; a < cnt; ++a) x[a] = zf[sup[a]];   // start: z on T
     std::vector<double> parts(h->rf_nparts);
     GemvDesc aw{h->rf_AT, kp, rows, kp, h->rf_x, h->rf_w, 0};
-    // f(v): uploads v into rf_x, leaves w = AT v in rf_w
+    GemvDesc awc{h->rf_AT, kp, rows, kp, h->rf_X, h->rf_W, 0, h->rf_xt};
+    // f(v): leaves w = AT v (logistic) or W = AT X(v) (softmax) on the device
     auto objective = [&](const std::vector<double>& v, double& f) -> int {
-        H_CUDA(h, cudaMemcpyAsync(h->rf_x, v.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
-        H_RC(h, launch_gemv(BICADMM_F64, &aw, 1, h->gemv_cap, st, 1));
-        H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, nullptr, nullptr, h->rf_obj, st));
+        if (sm) {
+            std::fill(Xh.begin(), Xh.end(), 0.0);
+            for (int64_t a = 0; a < cnt; ++a) Xh[a * C + sup[a] % C] = v[a];
+            H_CUDA(h, cudaMemcpyAsync(h->rf_X, Xh.data(), sizeof(double) * kp * C, cudaMemcpyHostToDevice, st));
+            H_RC(h, launch_gemv(BICADMM_F64, &awc, 1, h->gemv_cap, st, C));
+            H_RC(h, launch_rf_sm_rows(rows, C, h->rf_b, h->rf_W, nullptr, nullptr, h->rf_obj, st));
+        } else {
+            H_CUDA(h, cudaMemcpyAsync(h->rf_x, v.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
+            H_RC(h, launch_gemv(BICADMM_F64, &aw, 1, h->gemv_cap, st, 1));
+            H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, nullptr, nullptr, h->rf_obj, st));
+        }
         H_CUDA(h, cudaMemcpyAsync(parts.data(), h->rf_obj, sizeof(double) * parts.size(), cudaMemcpyDeviceToHost, st));
         H_CUDA(h, cudaStreamSynchronize(st));
-        double s = 0.0, xx = 0.0;
-        for (double p : parts) s += p;
+        double sum = 0.0, xx = 0.0;
+        for (double p : parts) sum += p;
         for (int64_t a = 0; a < kp; ++a) xx += v[a] * v[a];
-        f = s + 0.5 * lam * xx;
+        f = sum + 0.5 * lam * xx;
         return BICADMM_OK;
     };
     double f = 0.0;
@@ -1517,19 +1542,34 @@ static int do_refit_logistic(bicadmm_handle* h) {
     const int64_t ldf = rup(kp, 8);
     h->rf_newton = 0;
     for (int it = 0; it < 100; ++it) {
-        // gradient AT^T psi + lambda x and Hessian AT^T diag(s(1-s)) AT + lambda I at x (w = AT x)
-        H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, h->rf_psi, h->rf_sd, h->rf_obj, st));
         GemvTDesc gt = h->rf_gt;
-        gt.A = h->rf_AT; gt.lda = kp; gt.p = h->rf_psi; gt.delta = nullptr; gt.z = nullptr; gt.u = nullptr;
-        gt.r = h->rf_g; gt.partial = h->rf_part;
-        H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, 1));
-        H_RC(h, launch_rf_scale_rows(rows, kp, h->rf_AT, h->rf_sd, h->rf_BT, st));
-        H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+        gt.A = h->rf_AT; gt.lda = kp; gt.delta = nullptr; gt.z = nullptr; gt.u = nullptr; gt.partial = h->rf_part;
+        if (sm) {
+            H_RC(h, launch_rf_sm_rows(rows, C, h->rf_b, h->rf_W, h->rf_G, h->rf_P, h->rf_obj, st));
+            gt.p = h->rf_G; gt.r = h->rf_Y;
+            H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, C));   // Y = AT^T (P - E_y)
+            H_RC(h, launch_rf_sm_scale(rows, kp, C, h->rf_AT, h->rf_P, h->support, h->support_count, h->rf_BT, h->rf_U, st));
+            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_U, kp, 1.0, 0.0, h->rf_F2, ldf, false, st));
+            H_RC(h, launch_rf_sm_combine(kp, ldf, C, h->support, h->support_count, h->rf_F, h->rf_F2, st));
+        } else {
+            H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, h->rf_psi, h->rf_sd, h->rf_obj, st));
+            gt.p = h->rf_psi; gt.r = h->rf_g;
+            H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, 1));    // AT^T psi
+            H_RC(h, launch_rf_scale_rows(rows, kp, h->rf_AT, h->rf_sd, h->rf_BT, st));
+            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+        }
         // (padding columns >= |T| are zero in AT: their Hessian rows are lambda I, step 0)
         int rc = factor_inverse(kp, h->rf_F, ldf, h->rf_H, kp, BICADMM_F64, h->rf_ws, st);
-        if (rc) return fail(h, rc, "logistic refit: Hessian not positive definite");
-        H_CUDA(h, cudaMemcpyAsync(g.data(), h->rf_g, sizeof(double) * kp, cudaMemcpyDeviceToHost, st));
-        H_CUDA(h, cudaStreamSynchronize(st));
+        if (rc) return fail(h, rc, "refit: Hessian not positive definite");
+        if (sm) {
+            H_CUDA(h, cudaMemcpyAsync(Yh.data(), h->rf_Y, sizeof(double) * kp * C, cudaMemcpyDeviceToHost, st));
+            H_CUDA(h, cudaStreamSynchronize(st));
+            for (int64_t a = 0; a < kp; ++a) g[a] = a < cnt ? Yh[a * C + sup[a] % C] : 0.0;
+        } else {
+            H_CUDA(h, cudaMemcpyAsync(g.data(), h->rf_g, sizeof(double) * kp, cudaMemcpyDeviceToHost, st));
+            H_CUDA(h, cudaStreamSynchronize(st));
+        }
         for (int64_t a = 0; a < kp; ++a) g[a] += lam * x[a];
         // d = -H^{-1} g
         H_CUDA(h, cudaMemcpyAsync(h->rf_r, g.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
@@ -1549,13 +1589,14 @@ static int do_refit_logistic(bicadmm_handle* h) {
             for (int64_t a = 0; a < cnt; ++a) x[a] += d[a];
             break;
         }
+        const bool resolve = -gd > 1e-12 * (1.0 + std::fabs(f));   // as in the oracle (R29)
         double alpha = 1.0, fn = f;
         for (int ls = 0; ls < 60; ++ls, alpha *= 0.5) {
             for (int64_t a = 0; a < kp; ++a) xn[a] = a < cnt ? x[a] + alpha * d[a] : 0.0;
             H_RC(h, objective(xn, fn));
-            if (fn <= f + 1e-4 * alpha * gd) break;
+            if (!resolve || fn <= f + 1e-4 * alpha * gd) break;
         }
-        x = xn;   // rf_w holds AT x for the accepted point
+        x = xn;   // the device state (w / W) belongs to the accepted point
         f = fn;
     }
     H_CUDA(h, cudaMemcpyAsync(h->rf_x, x.data(), sizeof(double) * kp, cudaMemcpyHostToDevice, st));
@@ -1572,9 +1613,10 @@ static int do_finalize(bicadmm_handle* h) {
     k_scatter_support<<<(unsigned)((kk + 255) / 256), 256, 0, h->st>>>(h->z, h->support, h->support_count, h->x_final);
     BIC_LAUNCHED();
     if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
-    // logistic refit (DESIGN R29): single rank (the gathered support matrix is local)
-    if (h->prm.refit && h->loss == BICADMM_LOGISTIC && h->C == 1 && h->rf_AT && !(h->comm && h->comm->world > 1))
-        H_RC(h, do_refit_logistic(h));
+    // logistic / softmax refit (DESIGN R29): single rank (the gathered support matrix is local)
+    if (h->prm.refit && (h->loss == BICADMM_LOGISTIC || h->loss == BICADMM_SOFTMAX) && h->rf_AT &&
+        !(h->comm && h->comm->world > 1))
+        H_RC(h, do_refit_newton(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
     for (auto& L : h->blk) ax.push_back(GemvDesc{L.A, L.lda, L.m, L.nj, h->x_final + L.c0 * h->C, L.pobj, 0, L.xt});

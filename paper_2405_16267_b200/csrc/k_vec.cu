@@ -135,23 +135,23 @@ int launch_axpy_scaled(int64_t n, double a, const double* x, double* y, cudaStre
 template <typename T>
 __global__ void k_rf_gather(const T* __restrict__ A, int64_t lda, int64_t m, int64_t c0, int64_t nj,
                             const int64_t* __restrict__ sup, const int64_t* __restrict__ cnt, double* __restrict__ AT,
-                            int64_t kp, int64_t row_off) {
+                            int64_t kp, int64_t row_off, int C) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m * kp) return;
     const int64_t r = e / kp, a = e % kp;
     if (a >= *cnt) return;
-    const int64_t l = sup[a];
+    const int64_t l = sup[a] / C;   // entry l*C + c of vec(X) -> feature l
     if (l < c0 || l >= c0 + nj) return;
     AT[(row_off + r) * kp + a] = (double)A[r * lda + (l - c0)];
 }
 
 int launch_rf_gather(int dtype, const void* A, int64_t lda, int64_t m, int64_t c0, int64_t nj, const int64_t* sup,
-                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s) {
+                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s, int C) {
     const int64_t n = m * kp;
     if (n <= 0) return BICADMM_OK;
     const unsigned g = (unsigned)((n + 255) / 256);
-    if (dtype == BICADMM_F64) k_rf_gather<double><<<g, 256, 0, s>>>(static_cast<const double*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off);
-    else k_rf_gather<float><<<g, 256, 0, s>>>(static_cast<const float*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off);
+    if (dtype == BICADMM_F64) k_rf_gather<double><<<g, 256, 0, s>>>(static_cast<const double*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off, C);
+    else k_rf_gather<float><<<g, 256, 0, s>>>(static_cast<const float*>(A), lda, m, c0, nj, sup, cnt, AT, kp, row_off, C);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }
@@ -197,6 +197,85 @@ __global__ void k_rf_scale_rows(int64_t n, int64_t kp, const double* __restrict_
 int launch_rf_scale_rows(int64_t n, int64_t kp, const double* AT, const double* sd, double* BT, cudaStream_t s) {
     if (n * kp <= 0) return BICADMM_OK;
     k_rf_scale_rows<<<(unsigned)((n * kp + 255) / 256), 256, 0, s>>>(n, kp, AT, sd, BT);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// softmax rows: p = softmax(w_r) (C classes), objective partials logsumexp(w) - w_y,
+// G = p - e_y (gradient weights; null in objective-only mode) and P = p
+__global__ void __launch_bounds__(kRfThreads) k_rf_sm_rows(int64_t n, int C, const double* __restrict__ y,
+                                                           const double* __restrict__ W, double* __restrict__ G,
+                                                           double* __restrict__ P, double* __restrict__ objpart) {
+    __shared__ double scratch[32];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double f = 0.0;
+    if (r < n) {
+        const double* w = W + r * C;
+        double mx = w[0];
+        for (int c = 1; c < C; ++c) mx = fmax(mx, w[c]);
+        double se = 0.0;
+        for (int c = 0; c < C; ++c) se += exp(w[c] - mx);
+        const int yy = (int)y[r];
+        f = mx + log(se) - w[yy];
+        if (G) {
+            for (int c = 0; c < C; ++c) {
+                const double p = exp(w[c] - mx) / se;
+                P[r * C + c] = p;
+                G[r * C + c] = p - (c == yy ? 1.0 : 0.0);
+            }
+        }
+    }
+    f = block_sum(f, scratch);
+    if (threadIdx.x == 0) objpart[blockIdx.x] = f;
+}
+
+int launch_rf_sm_rows(int64_t n, int C, const double* y, const double* W, double* G, double* P, double* objpart,
+                      cudaStream_t s) {
+    if (n <= 0) return BICADMM_OK;
+    k_rf_sm_rows<<<(unsigned)((n + kRfThreads - 1) / kRfThreads), kRfThreads, 0, s>>>(n, C, y, W, G, P, objpart);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// softmax Hessian factors: BT[r][a] = sqrt(p_{r,c_a}) AT[r][a], U[r][a] = p_{r,c_a} AT[r][a]
+// (c_a = sup[a] % C; padding columns of AT are zero)
+__global__ void k_rf_sm_scale(int64_t n, int64_t kp, int C, const double* __restrict__ AT, const double* __restrict__ P,
+                              const int64_t* __restrict__ sup, const int64_t* __restrict__ cnt, double* __restrict__ BT,
+                              double* __restrict__ U) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * kp) return;
+    const int64_t r = e / kp, a = e % kp;
+    const double p = a < *cnt ? P[r * C + sup[a] % C] : 0.0;
+    BT[e] = sqrt(p) * AT[e];
+    U[e] = p * AT[e];
+}
+
+int launch_rf_sm_scale(int64_t n, int64_t kp, int C, const double* AT, const double* P, const int64_t* sup,
+                       const int64_t* cnt, double* BT, double* U, cudaStream_t s) {
+    if (n * kp <= 0) return BICADMM_OK;
+    k_rf_sm_scale<<<(unsigned)((n * kp + 255) / 256), 256, 0, s>>>(n, kp, C, AT, P, sup, cnt, BT, U);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// lower triangle: F1 <- [c_a == c_b] F1 - F2 (the softmax Hessian from its two Grams; the
+// ridge is already on F1's diagonal, padding rows/columns keep lambda I)
+__global__ void k_rf_sm_combine(int64_t kp, int64_t ldf, int C, const int64_t* __restrict__ sup,
+                                const int64_t* __restrict__ cnt, double* __restrict__ F1, const double* __restrict__ F2) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= kp * kp) return;
+    const int64_t a = e / kp, b = e % kp;
+    if (b > a) return;
+    const int64_t k = *cnt;
+    if (a >= k || b >= k) return;
+    const bool same = (sup[a] % C) == (sup[b] % C);
+    const double v = (same ? F1[a * ldf + b] : (a == b ? F1[a * ldf + b] : 0.0)) - F2[a * ldf + b];
+    F1[a * ldf + b] = v;
+}
+
+int launch_rf_sm_combine(int64_t kp, int64_t ldf, int C, const int64_t* sup, const int64_t* cnt, double* F1,
+                         const double* F2, cudaStream_t s) {
+    k_rf_sm_combine<<<(unsigned)((kp * kp + 255) / 256), 256, 0, s>>>(kp, ldf, C, sup, cnt, F1, F2);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }

@@ -208,7 +208,13 @@ int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStr
 int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s);
 // logistic refit on the support (k_vec.cu; DESIGN R29)
 int launch_rf_gather(int dtype, const void* A, int64_t lda, int64_t m, int64_t c0, int64_t nj, const int64_t* sup,
-                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s);
+                     const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s, int C = 1);
+int launch_rf_sm_rows(int64_t n, int C, const double* y, const double* W, double* G, double* P, double* objpart,
+                      cudaStream_t s);
+int launch_rf_sm_scale(int64_t n, int64_t kp, int C, const double* AT, const double* P, const int64_t* sup,
+                       const int64_t* cnt, double* BT, double* U, cudaStream_t s);
+int launch_rf_sm_combine(int64_t kp, int64_t ldf, int C, const int64_t* sup, const int64_t* cnt, double* F1,
+                         const double* F2, cudaStream_t s);
 int launch_rf_logit(int64_t n, const double* b, const double* w, double* psi, double* sd, double* objpart,
                     cudaStream_t s);
 int64_t rf_logit_parts(int64_t n);

@@ -388,3 +388,19 @@ def test_logistic_refit_matches_oracle(bc, orc, dtype, tol):
     T = ref["support"]
     z_on_T[T] = ref["z"][T]
     assert ref["objective"] <= orc.objective(orc.Problem(Aref, bref, orc.LOGISTIC, 1, np.array(cs)), 100.0, z_on_T)
+
+
+@pytest.mark.parametrize("C", [3, 10])
+def test_softmax_refit_matches_oracle(bc, orc, C):
+    # DESIGN R29 for softmax: entry-support Newton refit, GPU vs oracle at 1e-9
+    P = dg.generate(2, 400, 60, 12, "softmax", C=C, seed=31)
+    cs = dg.block_partition(60, 2)
+    prm = dict(kappa=12, max_outer=15, inner_fixed=4, refit=1, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "softmax", bc.Params(**prm), cs, C=P.C)
+    s.iterate(15)
+    rep = s.finalize()
+    ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.SOFTMAX, P.C, np.array(cs)),
+                  orc.Params(**prm))
+    assert s.support().tolist() == ref["support"].tolist()
+    assert _rel(s.get(bc.FIELD_X_FINAL), ref["x_final"]) <= 1e-9
+    assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
