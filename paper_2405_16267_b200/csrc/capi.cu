@@ -1328,7 +1328,9 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
                 uniform = uniform && want[li] == want[0];
             }
             // from the second outer iteration on, a fixed uniform schedule replays one CUDA graph
-            const bool use_graph = graph_enabled() && !replay && uniform && k >= 1 && !h->graph.failed;
+            // (single rank only: multi-rank runs keep the eager launches, NCCL outside graphs)
+            const bool use_graph = graph_enabled() && !replay && uniform && k >= 1 && !h->graph.failed &&
+                                   !(h->comm && h->comm->world > 1);
             static const bool gdbg = getenv("BICADMM_GRAPH_DEBUG") != nullptr;
             if (gdbg) fprintf(stderr, "bicadmm: outer %d use_graph %d (replay %d uniform %d failed %d)\n", k, (int)use_graph,
                               (int)replay, (int)uniform, (int)h->graph.failed);
