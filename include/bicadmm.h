@@ -156,9 +156,13 @@ typedef enum {
     BICADMM_FIELD_PHASE_MS = 12, /* double [BICADMM_NPHASE]: device time per phase accumulated while
                                     profiling is on (CUDA events on the handle's stream) */
     BICADMM_FIELD_PHASE_COUNT = 13, /* int64 [BICADMM_NPHASE]: kernel launches per phase while profiling */
-    BICADMM_FIELD_SWEEP_KIND = 14 /* int32 [2]: inner-sweep implementation chosen at setup (0 two-pass,
+    BICADMM_FIELD_SWEEP_KIND = 14, /* int32 [2]: inner-sweep implementation chosen at setup (0 two-pass,
                                      1-4 single-pass kernels k_fused, k_fused2, k_fused3, k_fused4) and
                                      the number of local Woodbury (fat) blocks */
+    BICADMM_FIELD_P_LOCAL = 15,  /* per local block in blocks[] order: p_ij = A_ij x_ij of the last sweep
+                                    (m_i*C each, concatenated; property checks at full size) */
+    BICADMM_FIELD_R_LOCAL = 16   /* per local block: r_ij = rho_l A_ij^T q + rho_c (z_j - u_ij) of the last
+                                    sweep (n_j*C each; x_ij = H_ij r_ij; tall blocks only) */
 } bicadmm_field;
 
 /* Phases timed by bicadmm_set_profiling:

@@ -25,7 +25,7 @@ LOSSES = {"ls": LS, "logistic": LOGISTIC, "softmax": SOFTMAX, "hinge": HINGE}
 F64, F32 = 0, 1
 (FIELD_Z, FIELD_S, FIELD_SCALARS, FIELD_X_LOCAL, FIELD_U_LOCAL, FIELD_SUPPORT, FIELD_X_FINAL,
  FIELD_TRACE, FIELD_WBAR, FIELD_NU, FIELD_INNER_COUNTS, FIELD_LAUNCHES, FIELD_PHASE_MS, FIELD_PHASE_COUNT,
- FIELD_SWEEP_KIND) = range(15)
+ FIELD_SWEEP_KIND, FIELD_P_LOCAL, FIELD_R_LOCAL) = range(17)
 NPHASE = 8
 PHASES = ("gemv_t_partial", "gemv_t_reduce", "h_apply", "gemv", "allreduce", "prox", "global_step", "fused_sweep")
 SWEEP_AUTO, SWEEP_TWO_PASS, SWEEP_FUSED = 0, 1, 2

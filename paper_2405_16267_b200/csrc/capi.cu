@@ -1744,6 +1744,18 @@ extern "C" int bicadmm_get(bicadmm_handle* h, int field, void* dst, size_t bytes
         }
         break;
     }
+    case BICADMM_FIELD_P_LOCAL:
+    case BICADMM_FIELD_R_LOCAL: {
+        std::vector<const LBlock*> order(h->blk.size());
+        for (auto& L : h->blk) order[L.user_index] = &L;
+        for (auto* L : order) {
+            const bool pf = field == BICADMM_FIELD_P_LOCAL;
+            pieces.push_back(pf ? L->p : L->r);
+            piece_sz.push_back(sizeof(double) * (pf ? L->m : L->nj) * h->C);
+            sz += piece_sz.back();
+        }
+        break;
+    }
     case BICADMM_FIELD_NU:
         for (auto& nd : h->nod) { pieces.push_back(nd.nu); piece_sz.push_back(sizeof(double) * nd.m * h->C); sz += piece_sz.back(); }
         break;
