@@ -119,6 +119,7 @@ struct Bump {  // 256-byte aligned bump allocator over the workspace (base may b
 };
 
 int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+constexpr int kLoopRows = 4096;   // outer iterations per device-loop launch
 
 // Static row split of all local rows over `units` equal ranges (one per CTA or CTA pair):
 // for each node, the first unit touching it and how many units touch it.
@@ -219,6 +220,16 @@ struct bicadmm_handle {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int32_t host_i32[2] = {};
     bool capturing = false;   // inside the stream capture of graph_outer
+    // device-resident solve loop (bicadmm_solve): a CUDA-graph while node around one outer
+    // iteration, terminated on the device; trace rows appended on the device
+    double* dtrace = nullptr;         // [kLoopRows][6]
+    int* dcount = nullptr;
+    struct Loop {
+        cudaGraphExec_t exec = nullptr;
+        int sweeps = -1;
+        int64_t launches = 0;
+        bool failed = false;
+    } loop;
     cudaStream_t cap_st = nullptr;   // private capture stream (the caller's may be the legacy stream)
     // per-phase profiling (bicadmm_set_profiling)
     bool prof = false;
@@ -432,6 +443,8 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     // setup scratch: FP64 Gram / factor workspace
     const int64_t ldg = rup(kdmax, 8);
     h->mask = b.arr<double>(len);
+    h->dtrace = b.arr<double>((int64_t)kLoopRows * 6);
+    h->dcount = b.arr<int>(2);
     if (((P->loss == BICADMM_LOGISTIC && C == 1) || P->loss == BICADMM_SOFTMAX) && h->prm.refit) {
         int64_t rows = 0;
         for (auto& nd : h->nod) rows += nd.m;
@@ -1139,7 +1152,7 @@ static int materialize_x(bicadmm_handle* h, const std::vector<int>& nodes) {
     return BICADMM_OK;
 }
 
-static int outer_step(bicadmm_handle* h) {
+static int outer_step(bicadmm_handle* h, bool readback = true) {
     const double rho_b = h->prm.alpha * h->prm.rho_c;
     cudaEvent_t oa = nullptr, ob = nullptr;
     const int64_t lo0 = g_launches.load();
@@ -1160,7 +1173,7 @@ static int outer_step(bicadmm_handle* h) {
         rec_event(h, ob);
         h->pending.push_back({6, oa, ob, g_launches.load() - lo0});
     }
-    H_CUDA(h, cudaMemcpyAsync(h->host_sc, h->sc, sizeof(OuterScalars), cudaMemcpyDeviceToHost, h->st));
+    if (readback) H_CUDA(h, cudaMemcpyAsync(h->host_sc, h->sc, sizeof(OuterScalars), cudaMemcpyDeviceToHost, h->st));
     return BICADMM_OK;
 }
 
@@ -1683,10 +1696,133 @@ extern "C" int bicadmm_finalize(bicadmm_handle* h, bicadmm_report* rep) {
     return BICADMM_OK;
 }
 
+// One thread: append (p_r, d_r, b_r, t, v, tau) to the device trace, and keep the while
+// node running until the residual test (15) passes or `limit` iterations were done.
+__global__ void k_loop_ctl(cudaGraphConditionalHandle hnd, const OuterScalars* __restrict__ sc,
+                           double* __restrict__ trace, int* __restrict__ count, double ep, double ed, double eb) {
+    const int c = count[0], limit = count[1];   // count[1]: iteration budget of this launch
+    double* row = trace + (int64_t)c * 6;
+    row[0] = sc->p_r; row[1] = sc->d_r; row[2] = sc->b_r; row[3] = sc->t; row[4] = sc->v; row[5] = sc->tau;
+    count[0] = c + 1;
+    const bool conv = sc->p_r <= ep && sc->d_r <= ed && sc->b_r <= eb;
+    cudaGraphSetConditional(hnd, (!conv && c + 1 < limit) ? 1u : 0u);
+}
+
+// Device-resident outer loop: the fixed-schedule outer iteration as the
+// body of a CUDA-graph while node; the loop ends on the device (converged or the iteration
+// budget), so the host waits once per launch instead of once per outer iteration.
+// Returns BICADMM_ERR_STATE when not applicable (the caller iterates from the host).
+static int solve_device_loop(bicadmm_handle* h) {
+    if (!graph_enabled() || h->prof || h->loop.failed || (h->comm && h->comm->world > 1) ||
+        h->prm.inner_fixed <= 0 || h->outer_done < 1 || h->converged)
+        return BICADMM_ERR_STATE;
+    if (!h->schedule.empty() && h->outer_done - h->sched_start < h->sched_rows) return BICADMM_ERR_STATE;
+    std::vector<int> want(h->nod.size(), h->prm.inner_fixed);
+    const int maxs = h->prm.inner_fixed;
+    auto& Lp = h->loop;
+    if (!Lp.exec || Lp.sweeps != maxs) {
+        if (Lp.exec) { cudaGraphExecDestroy(Lp.exec); Lp.exec = nullptr; }
+        if (!h->cap_st && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            Lp.failed = true;
+            return BICADMM_ERR_STATE;
+        }
+        cudaGraph_t g = nullptr;
+        cudaGraphConditionalHandle hnd = 0;
+        cudaGraphNode_t node = nullptr;
+        cudaGraphNodeParams cp{};
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess &&
+                  cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        if (ok) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = hnd;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+        }
+        const int64_t l0 = g_launches.load();
+        int rc = BICADMM_OK;
+        if (ok) {
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            cudaStream_t st0 = h->st;
+            h->st = h->cap_st;
+            ok = cudaStreamBeginCaptureToGraph(h->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
+                 cudaSuccess;
+            if (ok) {
+                h->capturing = true;
+                rc = enqueue_fixed(h, want, maxs);
+                if (!rc) rc = outer_step(h, false);
+                if (!rc) {
+                    k_loop_ctl<<<1, 1, 0, h->st>>>(hnd, h->sc, h->dtrace, h->dcount, h->prm.eps_p, h->prm.eps_d,
+                                                  h->prm.eps_b);
+                    count_launch();
+                }
+                cudaGraph_t out_g = nullptr;
+                ok = cudaStreamEndCapture(h->st, &out_g) == cudaSuccess && rc == BICADMM_OK;
+                h->capturing = false;
+            }
+            h->st = st0;
+        }
+        cudaGraphExec_t exec = nullptr;
+        if (ok && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) Lp.exec = exec;
+        if (g) cudaGraphDestroy(g);
+        const int64_t captured = g_launches.load() - l0;
+        g_launches.fetch_sub(captured);   // counted per executed iteration below
+        if (!Lp.exec) {
+            if (getenv("BICADMM_GRAPH_DEBUG")) fprintf(stderr, "bicadmm: device loop refused (rc %d)\n", rc);
+            cudaGetLastError();
+            h->dead = false;
+            h->err.clear();
+            h->pending.clear();
+            h->evused = 0;
+            Lp.failed = true;
+            return BICADMM_ERR_STATE;
+        }
+        Lp.launches = captured;
+        Lp.sweeps = maxs;
+    }
+    while (!h->converged && h->outer_done < h->prm.max_outer) {
+        const int budget = (int)std::min<int64_t>(kLoopRows, h->prm.max_outer - h->outer_done);
+        h->host_i32[0] = 0;
+        h->host_i32[1] = budget;
+        H_CUDA(h, cudaMemcpyAsync(h->dcount, h->host_i32, sizeof(int) * 2, cudaMemcpyHostToDevice, h->st));
+        H_CUDA(h, cudaGraphLaunch(Lp.exec, h->st));
+        int cnt = 0;
+        H_CUDA(h, cudaMemcpyAsync(&cnt, h->dcount, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+        H_CUDA(h, cudaStreamSynchronize(h->st));
+        std::vector<double> rows((size_t)cnt * 6);
+        if (cnt > 0)
+            H_CUDA(h, cudaMemcpy(rows.data(), h->dtrace, sizeof(double) * rows.size(), cudaMemcpyDeviceToHost));
+        H_CUDA(h, cudaMemcpy(h->host_sc, h->sc, sizeof(OuterScalars), cudaMemcpyDeviceToHost));
+        g_launches.fetch_add(Lp.launches * cnt);
+        for (int k = 0; k < cnt; ++k) {
+            const double* r = rows.data() + (size_t)k * 6;
+            h->trace.push_back({r[0], r[1], r[2], r[3], r[4], r[5]});
+            std::vector<int32_t> row(h->N, 0);
+            for (size_t li = 0; li < h->nod.size(); ++li) row[h->nod[li].node] = maxs;
+            h->inner_counts.insert(h->inner_counts.end(), row.begin(), row.end());
+            h->converged = r[0] <= h->prm.eps_p && r[1] <= h->prm.eps_d && r[2] <= h->prm.eps_b;
+        }
+        h->outer_done += cnt;
+        h->inner_total += (int64_t)cnt * maxs;
+        h->finalized = false;
+        if (cnt == 0) break;
+    }
+    return BICADMM_OK;
+}
+
 extern "C" int bicadmm_solve(bicadmm_handle* h, bicadmm_report* rep) {
     if (!h) return BICADMM_ERR_INVALID;
     if (h->dead) return BICADMM_ERR_STATE;
     H_CUDA(h, cudaEventRecord(h->e0, h->st));
+    if (!h->converged && h->outer_done < 1 && h->prm.max_outer > 0) {   // the loop graph starts at k >= 1
+        int rc = bicadmm_iterate(h, 1, nullptr);
+        if (rc) return rc;
+    }
+    if (!h->converged && h->outer_done < h->prm.max_outer) {
+        const int rc = solve_device_loop(h);
+        if (rc && rc != BICADMM_ERR_STATE) return rc;
+    }
     while (!h->converged && h->outer_done < h->prm.max_outer) {
         int rc = bicadmm_iterate(h, 1, nullptr);
         if (rc) return rc;
@@ -1831,6 +1967,7 @@ extern "C" int bicadmm_destroy(bicadmm_handle* h) {
     if (h->e1) cudaEventDestroy(h->e1);
     for (auto e : h->evpool) cudaEventDestroy(e);
     if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
+    if (h->loop.exec) cudaGraphExecDestroy(h->loop.exec);
     if (h->cap_st) cudaStreamDestroy(h->cap_st);
     delete h;
     return BICADMM_OK;

@@ -404,3 +404,29 @@ def test_softmax_refit_matches_oracle(bc, orc, C):
     assert s.support().tolist() == ref["support"].tolist()
     assert _rel(s.get(bc.FIELD_X_FINAL), ref["x_final"]) <= 1e-9
     assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
+
+
+def test_device_loop_solve_matches_host_loop(bc):
+    # bicadmm_solve runs the fixed-schedule outer loop as a CUDA-graph while node with
+    # device-side termination; it must reproduce the host-driven loop bit for bit
+    # (iterations, trace, z, support, objective)
+    import os
+    P = dg.generate(2, 100, 50, 5, "ls", seed=3)
+    cs = dg.block_partition(50, 1)
+    out = {}
+    for g in ("1", "0"):
+        os.environ["BICADMM_GRAPH"] = g
+        try:
+            s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls",
+                           bc.Params(kappa=5, max_outer=2000, inner_fixed=10, refit=1), cs)
+            rep = s.solve()
+            out[g] = (rep.outer_iters, rep.converged, s.trace(), s.z, s.support(), rep.objective,
+                      s.get(bc.FIELD_INNER_COUNTS, np.int32))
+            s.close()
+        finally:
+            del os.environ["BICADMM_GRAPH"]
+    a, b = out["1"], out["0"]
+    assert a[0] == b[0] and a[1] == b[1] == 1
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+    assert a[5] == b[5]
+    assert np.array_equal(a[6], b[6])
