@@ -46,6 +46,16 @@ int bicadmm_op_block_factor(int dtype, int64_t m, int64_t nj, const void* A, int
 int bicadmm_op_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda,
                     double alpha, double diag, double* G, int64_t ldg, void* stream);
 
+/* The same Gram on the 5th-generation tensor cores: FP64-accurate
+ * Ozaki-scheme emulation with exact int8 slices of the column-scaled A on tcgen05.mma
+ * kind::i8 (S = 8 slices: 56 bits below each column's maximum), TMEM accumulators, FP64 recombination.
+ * Writes the LOWER triangle of G = alpha A^T A + diag I (FP64, ldg >= nj); the upper triangle
+ * is left untouched.  ws: device scratch >= bicadmm_op_gram_tc_ws(dtype, m, nj) bytes
+ * (caller-owned).  Errors: BICADMM_ERR_INVALID on bad sizes or a short workspace. */
+size_t bicadmm_op_gram_tc_ws(int dtype, int64_t m, int64_t nj);
+int bicadmm_op_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag,
+                       double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream);
+
 /* a10 ((7b); DESIGN R3): wbar = wsum / N; exact (z,t) minimiser by the
  * weighted soft-threshold with tau the root of N rho_c tau = rho_b (psi(tau) - v).
  * z_prev receives the old z; out_host[0..3] = t, tau, ||z - z_prev||^2, psi(0). */

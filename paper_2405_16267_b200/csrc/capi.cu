@@ -164,6 +164,8 @@ struct bicadmm_handle {
            *wsum = nullptr, *x_final = nullptr, *node_sq = nullptr, *upart = nullptr, *gram = nullptr,
            *fws = nullptr, *node_obj = nullptr;
     int fbatch = 1;                          // blocks factored together (factor_inverse_batched)
+    void* gtc_ws = nullptr;                  // tcgen05 Gram scratch (int8 slices + column scales)
+    size_t gtc_bytes = 0;
     // logistic refit on the support (DESIGN R29): gathered support columns and Newton scratch
     int64_t rf_kp = 0, rf_rows = 0, rf_nparts = 0;
     double *rf_AT = nullptr, *rf_BT = nullptr, *rf_b = nullptr, *rf_w = nullptr, *rf_psi = nullptr,
@@ -549,6 +551,13 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         h->fbatch = std::max(1, fb);
         h->gram = b.arr<double>(h->gram_stride * h->fbatch);
         h->fws = b.arr<double>(h->fws_stride * h->fbatch);
+        // tcgen05 Ozaki-scheme Gram (k_gram_tc.cu) for tall blocks: slices of up to 32,768 rows
+        size_t gtc = 0;
+        if (gram_tc_enabled())
+            for (auto& L : h->blk)
+                if (!L.fat) gtc = std::max(gtc, gram_tc_scratch_bytes(P->dtype, L.m, L.nj));
+        h->gtc_bytes = gtc;
+        h->gtc_ws = gtc ? b.take(gtc) : nullptr;
     }
     return b.off + 256;
 }
@@ -912,7 +921,9 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             double* G = h->gram + k * h->gram_stride;
             if (L.fat)   // K = (c/rho_l) I + A A^T  (Woodbury, R27)
                 rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, G, ldg, h->st);
-            else         // F = rho_l A^T A + c I  (Eq. (24))
+            else if (h->gtc_ws)   // F = rho_l A^T A + c I  (Eq. (24)), tcgen05 Ozaki-scheme Gram
+                rc = launch_gram_tc(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, G, ldg, h->gtc_ws, h->gtc_bytes, h->st);
+            else         // F = rho_l A^T A + c I  (Eq. (24)), FP64 DMMA Gram
                 rc = launch_gram(P->dtype, L.m, L.nj, L.A, L.lda, R->rho_l, c, G, ldg, false, h->st);
             // packed H: the full FP64 inverse goes into the (consumed) Gram scratch, then packed
             jobs.push_back(FactorJob{L.kd, G, ldg, L.hpack ? (void*)G : L.H, L.hpack ? ldg : L.ldh,

@@ -1,0 +1,409 @@
+// k_gram_tc.cu -- FP64-accurate Gram G = A^T A on the 5th-generation tensor cores
+// (Ozaki-scheme emulation on tcgen05 kind::i8).
+//
+// sm_100a has no FP64 tcgen05 kind; the FP64 DMMA path (k_factor.cu) runs near its
+// ~40 TFLOP/s peak.  Here every column l of A is scaled by 2^-e_l (|A[:,l]| < 2^e_l) and
+// split exactly into S signed 7-bit slices,
+//     A[r,l] 2^-e_l = sum_{s=1..S} d_s[r,l] 2^-7s + eps,   d_s in [-127, 127], |eps| < 2^-7S
+// (S = 8: 56 bits below the column maximum, for FP64 and FP32 data alike), so that
+//     G[i,j] = 2^(e_i+e_j) sum_{s+t <= S+1} 2^-7(s+t) (D_s^T D_t)[i,j]     (+ O(2^-7(S+1)))
+// Each D_s^T D_t is an exact int8 x int8 -> int32 product on tcgen05.mma kind::i8; the
+// products of equal weight w = s + t accumulate in one TMEM accumulator (8 accumulators of
+// 128 x 64 int32 = all 512 TMEM columns), flushed to FP64 registers every 16,384 rows
+// (int32 headroom: 8 products x 127^2 x 16,384 < 2^31).  The weighted sum over w is formed
+// in FP64 in a fixed order (deterministic), scaled, and written as alpha G + diag I (lower
+// triangle).  Error per entry ~2^-56 m max|A_i| max|A_j| (FP64 data).
+//
+// Pipeline per CTA (one 128 x 64 tile of G, lower triangle of tiles):
+//   warp 5    : one thread issues the TMA copies (cp.async.bulk.tensor.2d, SWIZZLE_32B) of
+//               the S slices of 32 rows x (128 + 64) columns into a 4-stage ring
+//   warp 4    : one thread issues S(S+1)/2 tcgen05.mma (M 128, N 64, K 32) per stage,
+//               commits to the stage's "empty" barrier and, per 16,384-row round, to
+//               "acc_full"
+//   warps 0-3 : the TMEM epilogue (tcgen05.ld of the 8 accumulators per round)
+// The slices are produced once per block by k_oz_split (column-major int8, zero padded).
+#include <cuda.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bic {
+
+constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 32;   // tile M (columns i), N (columns j), K (rows per stage)
+constexpr int kOzSMax = 8;
+constexpr int kOzStages = 4;
+constexpr int kOzRoundStages = 16384 / kOzBK;         // stages per int32 accumulation round
+constexpr int kOzThreads = 192;                       // 4 epilogue warps, 1 MMA warp, 1 TMA warp
+constexpr size_t kOzStageBytes = (size_t)kOzSMax * (kOzBM + kOzBN) * kOzBK;   // 48 KB
+constexpr int kOzRowChunk = 32768;                    // rows of A split per launch pair
+
+__device__ __forceinline__ uint32_t oz_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ----------------------------------------------------------------------------- exponents
+// colmax[l] = max_r |A[r,l]| as order-preserving int64 bits (atomicMax: exact, deterministic)
+template <typename T>
+__global__ void k_oz_colmax(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t rows_per,
+                            unsigned long long* __restrict__ colmax) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n) return;
+    const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
+    double mx = 0.0;
+    for (int64_t r = r0; r < r1; ++r) mx = fmax(mx, fabs((double)A[r * lda + l]));
+    atomicMax(colmax + l, (unsigned long long)__double_as_longlong(mx));
+}
+
+// ----------------------------------------------------------------------------- split
+// Thread = (column l, 32 rows): slices written as out[s][l][r] (column-major, row stride
+// mp), 32 bytes per slice per thread.  Rows >= m and columns >= n are zero.
+template <typename T>
+__global__ void k_oz_split(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t r_begin,
+                           int64_t rows, const unsigned long long* __restrict__ colmax, int S, int8_t* __restrict__ out,
+                           int64_t np, int64_t mp) {
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t rg = (int64_t)blockIdx.y * 32;   // row group within this chunk
+    if (l >= np || rg >= mp) return;
+    int e = 0;
+    if (l < n) {
+        const double mx = __longlong_as_double((long long)colmax[l]);
+        e = mx > 0.0 ? ilogb(mx) + 1 : 0;           // |A[:, l]| < 2^e
+    }
+    uint32_t pk[kOzSMax][8];
+#pragma unroll
+    for (int s = 0; s < kOzSMax; ++s)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pk[s][q] = 0u;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const int64_t r = rg + k;
+        double a = 0.0;
+        if (l < n && r < rows && r_begin + r < m) a = scalbn((double)A[(r_begin + r) * lda + l], -e);
+#pragma unroll
+        for (int s = 0; s < kOzSMax; ++s) {
+            if (s < S) {
+                const double t = a * 128.0;               // exact
+                const double d = trunc(t);                // |d| <= 127
+                a = t - d;                                // exact
+                const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
+                pk[s][k >> 2] |= byte << (8 * (k & 3));
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < kOzSMax; ++s) {
+        if (s >= S) break;
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * np + l) * mp + rg);
+        dst[0] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
+        dst[1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
+    }
+}
+
+// ----------------------------------------------------------------------------- GEMM
+// Operands by TMA (cp.async.bulk.tensor.2d, SWIZZLE_32B: one K = 32-byte row per column,
+// 8-column atoms of 256 B), 4-stage ring, one tcgen05.mma (M 128, N 64, K 32) per slice
+// pair per stage.
+__device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major layouts)
+    d |= (uint64_t)(256 >> 4) << 32;           // SBO: 8 columns x 32 B
+    d |= (uint64_t)1 << 46;                    // descriptor version 1 (sm_100)
+    d |= (uint64_t)6 << 61;                    // SWIZZLE_32B
+    return d;
+}
+__device__ __forceinline__ void oz_mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    for (long long it = 0; !ok; ++it) {
+        asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                     : "=r"(ok) : "r"(oz_smem(b)), "r"(parity) : "memory");
+        if (it > (1ll << 28)) asm volatile("trap;");
+    }
+}
+// long waits (the epilogue waits a whole accumulation round): back off with nanosleep so
+// the spinning warps do not take issue slots from the MMA and TMA threads
+__device__ __forceinline__ void oz_mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    for (long long it = 0; !ok; ++it) {
+        asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                     : "=r"(ok) : "r"(oz_smem(b)), "r"(parity) : "memory");
+        if (!ok) __nanosleep(2000);
+        if (it > (1ll << 26)) asm volatile("trap;");
+    }
+}
+__device__ __forceinline__ void oz_mbar_arrive(uint64_t* b) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(oz_smem(b)) : "memory");
+}
+__device__ __forceinline__ void oz_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
+        "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+          "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]),
+          "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]),
+          "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
+          "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+        : "r"(taddr));
+}
+
+struct OzArgs {
+    int64_t np, mp, n;       // padded columns, padded rows of this chunk, true columns
+    const unsigned long long* colmax;
+    int S;
+    double alpha, diag;
+    double* G;
+    int64_t ldg;
+    int accumulate;          // add into G (row chunks after the first); else overwrite
+};
+
+__global__ void __launch_bounds__(kOzThreads, 1)
+    k_oz_gram(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ OzArgs a) {
+    extern __shared__ __align__(1024) uint8_t oz_sm_raw[];
+    uint8_t* oz_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_sm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kOzStages], empty[kOzStages], acc_full, acc_empty;
+    __shared__ uint32_t tmem_base;
+    // tile (bi, bj): column block bi of 128 (rows of G), bj of 64 with 64 bj < 128 (bi + 1)
+    int64_t t = blockIdx.x, bi = 0;
+    while (t >= 2 * bi + 2) { t -= 2 * bi + 2; ++bi; }
+    const int64_t bj = t;
+    const int64_t i0 = bi * kOzBM, j0 = bj * kOzBN;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int S = a.S;
+    const int nstage = (int)(a.mp / kOzBK);
+    const uint32_t bytes_stage = (uint32_t)(S * (kOzBM + kOzBN) * kOzBK);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_smem(&tmem_base)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kOzStages; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&empty[s])));
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&acc_full)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_smem(&acc_empty)), "r"(128));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const int nround = (nstage + kOzRoundStages - 1) / kOzRoundStages;
+
+    if (warp == 5) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            for (int st = 0; st < nstage; ++st) {
+                const int sb = st % kOzStages;
+                if (st >= kOzStages) oz_mbar_wait(&empty[sb], (uint32_t)((st / kOzStages - 1) & 1));
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_smem(&full[sb])),
+                             "r"(bytes_stage) : "memory");
+                uint8_t* base = oz_sm + (size_t)sb * kOzStageBytes;
+                const int k0 = st * kOzBK;
+#pragma unroll
+                for (int s = 0; s < kOzSMax; ++s) {
+                    const int ra = (int)(s * a.np + i0), rbb = (int)(s * a.np + j0);   // S == kOzSMax
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                        ::"r"(oz_smem(base + (size_t)s * kOzBM * kOzBK)), "l"(&tmA), "r"(k0), "r"(ra),
+                          "r"(oz_smem(&full[sb])) : "memory");
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                        ::"r"(oz_smem(base + (size_t)kOzSMax * kOzBM * kOzBK + (size_t)s * kOzBN * kOzBK)), "l"(&tmB),
+                          "r"(k0), "r"(rbb), "r"(oz_smem(&full[sb])) : "memory");
+                }
+            }
+        }
+    } else if (warp == 4) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            // idesc: S32 accumulate, s8 x s8, K-major A and B, N = 64, M = 128
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) |
+                                   ((uint32_t)(kOzBM >> 4) << 24);
+            const uint32_t smem0 = oz_smem(oz_sm);
+            int st = 0;
+            for (int rd = 0; rd < nround; ++rd) {
+                if (rd > 0) oz_mbar_wait(&acc_empty, (uint32_t)((rd - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const int st_end = (rd + 1) * kOzRoundStages < nstage ? (rd + 1) * kOzRoundStages : nstage;
+                const int st_begin = st;
+                for (; st < st_end; ++st) {
+                    const int sb = st % kOzStages;
+                    oz_mbar_wait(&full[sb], (uint32_t)((st / kOzStages) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    // descriptors: the start-address field is bits [0,14) in 16-byte units, so the
+                    // slice tiles of this stage are fixed offsets from the stage's base descriptor
+                    const uint64_t dA0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes));
+                    const uint64_t dB0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes) + (uint32_t)(kOzSMax * kOzBM * kOzBK));
+                    const uint32_t first = st == st_begin ? 1u : 0u;
+#pragma unroll
+                    for (int sa = 1; sa <= kOzSMax; ++sa)
+#pragma unroll
+                        for (int sbk = 1; sbk <= kOzSMax; ++sbk) {
+                            if (sa + sbk > kOzSMax + 1) continue;
+                            const int w = sa + sbk;
+                            const uint32_t dt = tmem + (uint32_t)((w - 2) * kOzBN);
+                            const uint64_t da = dA0 + (uint64_t)(((sa - 1) * kOzBM * kOzBK) >> 4);
+                            const uint64_t db = dB0 + (uint64_t)(((sbk - 1) * kOzBN * kOzBK) >> 4);
+                            // the first product of each weight in a round overwrites its accumulator
+                            const uint32_t accum = (sa == 1) ? (first ^ 1u) : 1u;
+                            asm volatile(
+                                "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(dt),
+                                "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                        }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        oz_smem(&empty[sb])));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    oz_smem(&acc_full)));
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 0-3)
+        double acc[kOzBN];
+#pragma unroll
+        for (int c = 0; c < kOzBN; ++c) acc[c] = 0.0;
+        for (int rd = 0; rd < nround; ++rd) {
+            oz_mbar_wait_sleep(&acc_full, (uint32_t)(rd & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
+            for (int w = 2; w <= S + 1; ++w) {   // fixed order w = 2 .. S + 1
+                uint32_t v[64];
+                oz_ld64(lane_addr + (uint32_t)((w - 2) * kOzBN), v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const double sc = ldexp(1.0, -7 * w);
+#pragma unroll
+                for (int c = 0; c < kOzBN; ++c) acc[c] = fma((double)(int32_t)v[c], sc, acc[c]);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            oz_mbar_arrive(&acc_empty);
+        }
+        // write alpha 2^(e_i + e_j) acc (+ diag on i == j), lower triangle
+        const int64_t i = i0 + 32 * warp + lane;
+        if (i < a.n) {
+            const double mi = __longlong_as_double((long long)a.colmax[i]);
+            const int ei = mi > 0.0 ? ilogb(mi) + 1 : 0;
+            double* grow = a.G + i * a.ldg;
+#pragma unroll 4
+            for (int c = 0; c < kOzBN; ++c) {
+                const int64_t j = j0 + c;
+                if (j > i || j >= a.n) continue;
+                const double mj = __longlong_as_double((long long)a.colmax[j]);
+                const int ej = mj > 0.0 ? ilogb(mj) + 1 : 0;
+                double v = a.alpha * ldexp(acc[c], ei + ej);
+                if (a.accumulate) v += grow[j];
+                else if (i == j) v += a.diag;
+                grow[j] = v;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ----------------------------------------------------------------------------- host
+static int64_t oz_rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+size_t gram_tc_scratch_bytes(int dtype, int64_t m, int64_t nj) {
+    (void)dtype;
+    const int S = kOzSMax;
+    const int64_t np = oz_rup(nj, kOzBM), rows = m < kOzRowChunk ? m : kOzRowChunk;
+    const int64_t mp = oz_rup(rows, kOzBK);
+    return (size_t)S * np * mp + sizeof(unsigned long long) * (size_t)np + 1024;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn oz_encode() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)f;
+    }();
+    return fn;
+}
+
+// 2-D map over the slices [S * np rows (slice, column)] x [mp bytes (rows of A)], box
+// {32 bytes, box_rows}, 32-byte swizzle (the UMMA K-major SWIZZLE_32B layout)
+static int oz_map(CUtensorMap* map, int8_t* sl, int64_t S, int64_t np, int64_t mp, uint32_t box_rows) {
+    EncodeTiledFn enc = oz_encode();
+    if (!enc) return BICADMM_ERR_CUDA;
+    const cuuint64_t dims[2] = {(cuuint64_t)mp, (cuuint64_t)(S * np)};
+    const cuuint64_t strides[1] = {(cuuint64_t)mp};
+    const cuuint32_t box[2] = {(cuuint32_t)kOzBK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, sl, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? BICADMM_OK : BICADMM_ERR_CUDA;
+}
+
+bool gram_tc_enabled() {
+    static const bool on = [] { const char* e = getenv("BICADMM_GRAM_TC"); return !(e && atoi(e) == 0); }();
+    return on;
+}
+
+int launch_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag, double* G,
+                   int64_t ldg, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+    if (m <= 0 || nj <= 0) return BICADMM_OK;
+    if (scratch_bytes < gram_tc_scratch_bytes(dtype, m, nj)) return BICADMM_ERR_INVALID;
+    const int S = kOzSMax;   // FP32 data too: entries far below their column maximum need the bits
+    const int64_t np = oz_rup(nj, kOzBM);
+    const int64_t rows_max = m < kOzRowChunk ? m : kOzRowChunk;
+    const int64_t mp_max = oz_rup(rows_max, kOzBK);
+    int8_t* sl = static_cast<int8_t*>(scratch);
+    unsigned long long* colmax = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(scratch) + oz_rup((int64_t)S * np * mp_max, 256));
+    static bool attr = false;
+    const size_t smem = kOzStages * kOzStageBytes + 1024;   // + alignment slack
+    if (!attr) {
+        BIC_CUDA(cudaFuncSetAttribute(k_oz_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    // column scales over all rows
+    BIC_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * np, s));
+    {
+        const int64_t rows_per = 2048;
+        dim3 g((unsigned)((nj + 255) / 256), (unsigned)((m + rows_per - 1) / rows_per));
+        if (dtype == BICADMM_F64) k_oz_colmax<double><<<g, 256, 0, s>>>(static_cast<const double*>(A), lda, m, nj, rows_per, colmax);
+        else k_oz_colmax<float><<<g, 256, 0, s>>>(static_cast<const float*>(A), lda, m, nj, rows_per, colmax);
+        BIC_LAUNCHED();
+    }
+    const int64_t ntb = np / kOzBM;
+    const int64_t tiles = ntb * (ntb + 1);   // sum over bi of (2 bi + 2)
+    for (int64_t r_begin = 0; r_begin < m; r_begin += kOzRowChunk) {
+        const int64_t rows = m - r_begin < kOzRowChunk ? m - r_begin : kOzRowChunk;
+        const int64_t mp = oz_rup(rows, kOzBK);
+        dim3 gs((unsigned)((np + 127) / 128), (unsigned)(mp / 32));
+        if (dtype == BICADMM_F64)
+            k_oz_split<double><<<gs, 128, 0, s>>>(static_cast<const double*>(A), lda, m, nj, r_begin, rows, colmax, S, sl, np, mp);
+        else
+            k_oz_split<float><<<gs, 128, 0, s>>>(static_cast<const float*>(A), lda, m, nj, r_begin, rows, colmax, S, sl, np, mp);
+        BIC_LAUNCHED();
+        CUtensorMap tmA, tmB;
+        int rc = oz_map(&tmA, sl, S, np, mp, kOzBM);
+        if (!rc) rc = oz_map(&tmB, sl, S, np, mp, kOzBN);
+        if (rc) return rc;
+        OzArgs oa{};
+        oa.np = np; oa.mp = mp; oa.n = nj; oa.colmax = colmax; oa.S = S;
+        oa.alpha = alpha; oa.diag = diag; oa.G = G; oa.ldg = ldg; oa.accumulate = r_begin > 0;
+        k_oz_gram<<<(unsigned)tiles, kOzThreads, smem, s>>>(tmA, tmB, oa);
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
+}  // namespace bic

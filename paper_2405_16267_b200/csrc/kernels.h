@@ -85,6 +85,12 @@ int launch_loss(int loss, int dtype, int C, ProxNode* nodes, int nn, cudaStream_
 
 // ---------------------------------------------------------------- dense factor (a0)
 // F = alpha A^T A + diag I (lower triangle or full) into FP64 G (ldg).
+// FP64-accurate Gram on tcgen05 kind::i8 (Ozaki slices, k_gram_tc.cu): lower triangle of
+// alpha A^T A + diag I into G (FP64, ldg); scratch of gram_tc_scratch_bytes() (slices + scales)
+size_t gram_tc_scratch_bytes(int dtype, int64_t m, int64_t nj);
+bool gram_tc_enabled();
+int launch_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag, double* G,
+                   int64_t ldg, void* scratch, size_t scratch_bytes, cudaStream_t s);
 int launch_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
                 double diag, double* G, int64_t ldg, bool full, cudaStream_t s);
 // K = alpha A A^T + diag I (m x m, lower triangle or full) into FP64 G (ldg): the Woodbury

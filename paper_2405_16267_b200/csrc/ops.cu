@@ -88,6 +88,16 @@ extern "C" int bicadmm_op_gram(int dtype, int64_t m, int64_t nj, const void* A, 
     return launch_gram(dtype, m, nj, A, lda, alpha, diag, G, ldg, true, (cudaStream_t)stream);
 }
 
+extern "C" size_t bicadmm_op_gram_tc_ws(int dtype, int64_t m, int64_t nj) {
+    return (m < 1 || nj < 1) ? 0 : gram_tc_scratch_bytes(dtype, m, nj);
+}
+
+extern "C" int bicadmm_op_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
+                                  double diag, double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
+    if (m < 1 || nj < 1 || lda < nj || !A || !G || ldg < nj || !ws) return BICADMM_ERR_INVALID;
+    return launch_gram_tc(dtype, m, nj, A, lda, alpha, diag, G, ldg, ws, ws_bytes, (cudaStream_t)stream);
+}
+
 extern "C" int bicadmm_op_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s,
                              double v, double* wbar, double* z, double* z_prev, double* out_host, void* stream) {
     if (len < 1 || N < 1 || !wsum || !s || !wbar || !z || !z_prev || !out_host) return BICADMM_ERR_INVALID;

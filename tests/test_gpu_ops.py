@@ -145,6 +145,31 @@ def test_gram(bc, m, nj):
     assert np.max(np.abs(G.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("m,nj,dt", [(33, 5, "f64"), (517, 70, "f64"), (2000, 129, "f64"), (40000, 300, "f64"),
+                                     (3000, 200, "f32"), (70001, 64, "f64")])
+def test_gram_tc(bc, m, nj, dt):
+    # tcgen05 kind::i8 Ozaki-scheme Gram (lower triangle) vs the FP64 definition; columns of
+    # very different magnitudes (per-column scaling), ragged sizes, several 32768-row chunks
+    rng = np.random.default_rng(m + nj)
+    An = rng.normal(size=(m, -(-nj // 4) * 4)) * np.exp(rng.uniform(-6, 6, size=-(-nj // 4) * 4))
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    A = torch.tensor(An, device="cuda", dtype=tdt)
+    An = A.double().cpu().numpy()[:, :nj]
+    G = torch.full((nj, nj), 7.0, dtype=torch.float64, device="cuda")
+    code = bc.F64 if dt == "f64" else bc.F32
+    wsb = bc.lib().bicadmm_op_gram_tc_ws(code, m, nj)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    bc.check(bc.lib().bicadmm_op_gram_tc(code, m, nj, _p(A), A.stride(0), 2.0, 0.5, _p(G), nj, _p(ws), wsb, _s()))
+    torch.cuda.synchronize()
+    Gn = G.cpu().numpy()
+    ref = 2.0 * An.T @ An + 0.5 * np.eye(nj)
+    lo = np.tril_indices(nj)
+    d = np.sqrt(np.abs(np.diag(ref)))
+    err = np.abs(Gn - ref)[lo] / np.outer(d, d)[lo]     # relative to sqrt(G_ii G_jj)
+    assert np.max(err) <= 1e-13
+    assert np.all(Gn[np.triu_indices(nj, 1)] == 7.0)     # upper triangle untouched
+
+
 ZT_CASES = []
 _rng = np.random.default_rng(42)
 for _k in range(12):
