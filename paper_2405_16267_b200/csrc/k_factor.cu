@@ -11,6 +11,8 @@
 //   H = W^T W                       (DMMA, triangular K range, mirrored)
 // FP64 tensor cores exist on sm_100a only as mma.sync DMMA; tcgen05 has no f64
 // kind.  In FP32 mode the factor is still built in FP64 and H rounded once.
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -264,10 +266,157 @@ static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 size_t factor_ws_doubles(int64_t nj) {
     const int64_t ld = round_up(nj, 8);
-    return (size_t)(ld * nj + NB * ld + 8);
+    // W (nj x ld), the recursion's panel scratch (<= (nj/2 + NB) x ld), info
+    return (size_t)(ld * nj + (nj / 2 + NB + 8) * ld + 8);
+}
+
+// ------------------------------------------------------------------ recursive factor
+// chol_inv(F, n) -> L (in F, lower) and W = L^{-1} (in W), all jobs in lockstep (equal n):
+//   n <= NB : k_chol_diag
+//   else    : n1 = NB * ceil(n / 2 / NB), n2 = n - n1
+//             (L11, W11) = chol_inv(F11)
+//             L21 = F21 W11^T                (GEMM, via scratch X)
+//             F22 -= L21 L21^T               (lower tiles)
+//             (L22, W22) = chol_inv(F22)
+//             W21 = -W22 (L21 W11)           (two GEMMs, via X)
+// The same flops as the blocked right-looking factor + blocked inverse, but in GEMMs of
+// size n/2, n/4, ... instead of rank-64 updates (which are bound by the C read/write).
+struct RecJob {
+    double* F;   // job's F at (0, 0), leading dim ldf
+    int64_t ldf;
+    double* W;   // job's W at (0, 0), leading dim ldw
+    int64_t ldw;
+    double* X;   // scratch (>= (n/2 + NB) x ldw)
+    int* info;
+};
+
+static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStream_t s) {
+    if (n <= NB) {
+        DiagBatch db{};
+        for (int k = 0; k < nj; ++k) {
+            db.F[k] = J[k].F + off * J[k].ldf + off; db.ldf[k] = J[k].ldf;
+            db.Wd[k] = J[k].W + off * J[k].ldw + off; db.ldw[k] = J[k].ldw;
+            db.kn[k] = (int)n; db.info[k] = J[k].info;
+        }
+        k_chol_diag<<<nj, kDiagThreads, sizeof(double) * 2 * NB * (NB + 1), s>>>(db);
+        BIC_LAUNCHED();
+        return BICADMM_OK;
+    }
+    int64_t n1 = (n / 2 + NB - 1) / NB * NB;
+    if (n1 >= n) n1 = n - NB;
+    const int64_t n2 = n - n1;
+    int rc = chol_inv_rec(J, nj, n1, off, s);
+    if (rc) return rc;
+    GemmArgs ga[kMaxBatch];
+    // X = F21 W11^T  (n2 x n1 x n1): A(i,k) = F21[i][k] (K-fast), B(k,j) = W11[j][k] (K-fast)
+    for (int k = 0; k < nj; ++k) {
+        GemmArgs g{};
+        g.M = n2; g.N = n1; g.K = n1; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+        g.A = J[k].F + (off + n1) * J[k].ldf + off; g.lda = J[k].ldf;
+        g.B = J[k].W + off * J[k].ldw + off; g.ldb = J[k].ldw;
+        g.C = J[k].X; g.ldc = J[k].ldw;
+        ga[k] = g;
+    }
+    rc = gemm_batched<double, double, true, true>(ga, nj, s);
+    if (rc) return rc;
+    for (int k = 0; k < nj; ++k)   // L21 = X
+        BIC_CUDA(cudaMemcpy2DAsync(J[k].F + (off + n1) * J[k].ldf + off, sizeof(double) * J[k].ldf, J[k].X,
+                                   sizeof(double) * J[k].ldw, sizeof(double) * n1, n2, cudaMemcpyDeviceToDevice, s));
+    // F22 -= L21 L21^T (lower tiles): A(i,k) = L21[i][k], B(k,j) = L21[j][k]
+    for (int k = 0; k < nj; ++k) {
+        GemmArgs g{};
+        g.M = n2; g.N = n2; g.K = n1; g.alpha = -1.0; g.beta = 1.0; g.diag = 0.0;
+        g.A = J[k].F + (off + n1) * J[k].ldf + off; g.lda = J[k].ldf;
+        g.B = g.A; g.ldb = J[k].ldf;
+        g.C = J[k].F + (off + n1) * J[k].ldf + off + n1; g.ldc = J[k].ldf; g.lower_only = 1;
+        ga[k] = g;
+    }
+    rc = gemm_batched<double, double, true, true>(ga, nj, s);
+    if (rc) return rc;
+    rc = chol_inv_rec(J, nj, n2, off + n1, s);
+    if (rc) return rc;
+    // X = L21 W11 (n2 x n1 x n1): A(i,k) = L21[i][k], B(k,j) = W11[k][j] (N-fast)
+    for (int k = 0; k < nj; ++k) {
+        GemmArgs g{};
+        g.M = n2; g.N = n1; g.K = n1; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+        g.A = J[k].F + (off + n1) * J[k].ldf + off; g.lda = J[k].ldf;
+        g.B = J[k].W + off * J[k].ldw + off; g.ldb = J[k].ldw;
+        g.C = J[k].X; g.ldc = J[k].ldw;
+        ga[k] = g;
+    }
+    rc = gemm_batched<double, double, true, false>(ga, nj, s);
+    if (rc) return rc;
+    // W21 = -W22 X (n2 x n1 x n2): A(i,k) = W22[i][k], B(k,j) = X[k][j]
+    for (int k = 0; k < nj; ++k) {
+        GemmArgs g{};
+        g.M = n2; g.N = n1; g.K = n2; g.alpha = -1.0; g.beta = 0.0; g.diag = 0.0;
+        g.A = J[k].W + (off + n1) * J[k].ldw + off + n1; g.lda = J[k].ldw;
+        g.B = J[k].X; g.ldb = J[k].ldw;
+        g.C = J[k].W + (off + n1) * J[k].ldw + off; g.ldc = J[k].ldw;
+        ga[k] = g;
+    }
+    return gemm_batched<double, double, true, false>(ga, nj, s);
+}
+
+static bool factor_rec_enabled() {
+    static const bool on = [] { const char* e = getenv("BICADMM_FACTOR_REC"); return !(e && atoi(e) == 0); }();
+    return on;
+}
+
+static int factor_inverse_rec(const FactorJob* jobs, int njobs, cudaStream_t s) {
+    const int64_t n = jobs[0].n;
+    const int hdtype = jobs[0].hdtype;
+    RecJob J[kMaxBatch];
+    for (int k = 0; k < njobs; ++k) {
+        if (jobs[k].n != n || jobs[k].hdtype != hdtype) return BICADMM_ERR_INVALID;
+        const int64_t ldw = round_up(n, 8);
+        J[k].F = jobs[k].G; J[k].ldf = jobs[k].ldg;
+        J[k].W = jobs[k].ws; J[k].ldw = ldw;
+        J[k].X = jobs[k].ws + ldw * n;
+        J[k].info = reinterpret_cast<int*>(J[k].X + (n / 2 + NB + 8) * ldw);
+        BIC_CUDA(cudaMemsetAsync(J[k].W, 0, sizeof(double) * (size_t)(ldw * n), s));
+        BIC_CUDA(cudaMemsetAsync(J[k].info, 0, sizeof(int), s));
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        BIC_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(double) * 2 * NB * (NB + 1))));
+        attr_set = true;
+    }
+    int rc = chol_inv_rec(J, njobs, n, 0, s);
+    if (rc) return rc;
+    GemmArgs ga[kMaxBatch];
+    for (int k = 0; k < njobs; ++k) {   // H = W^T W (W lower: K range from max(m0, n0)); lower tiles mirrored
+        GemmArgs g{};
+        g.M = n; g.N = n; g.K = n; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
+        g.A = J[k].W; g.lda = J[k].ldw; g.B = J[k].W; g.ldb = J[k].ldw; g.C = jobs[k].H; g.ldc = jobs[k].ldh;
+        g.lower_only = 1; g.mirror = 1; g.tri_k = 1;
+        ga[k] = g;
+    }
+    rc = hdtype == BICADMM_F64 ? gemm_batched<double, double, false, false>(ga, njobs, s)
+                               : gemm_batched<double, float, false, false>(ga, njobs, s);
+    if (rc) return rc;
+    int hinfo[kMaxBatch] = {};
+    for (int k = 0; k < njobs; ++k) BIC_CUDA(cudaMemcpyAsync(&hinfo[k], J[k].info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BIC_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < njobs; ++k)
+        if (hinfo[k]) return BICADMM_ERR_INVALID;
+    return BICADMM_OK;
 }
 
 int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s) {
+    if (njobs > 0 && factor_rec_enabled()) {
+        // recursive (large-GEMM) variant, one lockstep batch per distinct size
+        std::vector<FactorJob> rest(jobs, jobs + njobs);
+        while (!rest.empty()) {
+            std::vector<FactorJob> same, other;
+            for (auto& j : rest) (j.n == rest[0].n && j.hdtype == rest[0].hdtype && same.size() < kMaxBatch ? same : other).push_back(j);
+            const int rc = factor_inverse_rec(same.data(), (int)same.size(), s);
+            if (rc) return rc;
+            rest.swap(other);
+        }
+        return BICADMM_OK;
+    }
     if (njobs <= 0) return BICADMM_OK;
     if (njobs > kMaxBatch) {
         for (int b = 0; b < njobs; b += kMaxBatch) {
