@@ -302,33 +302,53 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        dA = [a.to("cuda", non_blocking=True) for a in hostA]
-        db = [b.to("cuda", non_blocking=True) for b in hostb]
-        b_all2 = [None] * N
-        blocks2 = []
-        for k in range(nl):
-            b_all2[rank * nl + k] = db[k]
-            for j in range(M):
-                blocks2.append((rank * nl + k, j, dA[k][:, cs[j]:cs[j + 1]]))
-        s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False, C=C)
-        for _ in range(args.steps):
-            s2.iterate(1)          # each step reads back its 6 residual scalars
-        z = s2.z                   # D2H of the result
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
+        cps = torch.cuda.Stream()
+
+        def e2e_once():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            # node k's H2D on a copy stream, one ready event per node: setup's Gram of node k waits on
+            # its own event only (bicadmm_block.ready_event), so later copies overlap earlier Grams
+            cps.wait_stream(stream)
+            dA, db, evs = [], [], []
+            with torch.cuda.stream(cps):
+                for k in range(nl):
+                    dA.append(hostA[k].to("cuda", non_blocking=True))
+                    db.append(hostb[k].to("cuda", non_blocking=True))
+                    ev = torch.cuda.Event()
+                    ev.record(cps)
+                    evs.append(ev)
+            for t_ in dA + db:
+                t_.record_stream(stream)
+            b_all2 = [None] * N
+            blocks2 = []
+            for k in range(nl):
+                b_all2[rank * nl + k] = db[k]
+                for j in range(M):
+                    blocks2.append((rank * nl + k, j, dA[k][:, cs[j]:cs[j + 1]], evs[k]))
+            s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False, C=C)
+            for _ in range(args.steps):
+                s2.iterate(1)          # each step reads back its 6 residual scalars
+            z = s2.z                   # D2H of the result
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ems = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ems = float(t.item())
+            s2.close()
+            return ems, z
+
+        e2e_once()                 # untimed warm-up pass (first-use costs of the copy stream)
         if world > 1:
-            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            dist.barrier()
+        ems, z = e2e_once()
         h2d = sum(a.numel() * a.element_size() for a in hostA) + sum(b.numel() * b.element_size() for b in hostb)
         e2e = {"value": N * sweeps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / args.steps),
                "d2h_bytes_per_step": int((6 * 8 * args.steps + z.nbytes) / args.steps),
-               "ms_total": ems, "includes": "H2D of A,b + setup (Gram+factor) + steps + D2H of z"}
-        s2.close()
+               "ms_total": ems, "includes": "H2D of A,b (per-node copy stream, overlapping setup's Gram) + setup (Gram+factor) + steps + D2H of z; second of two passes"}
 
     ttt = None
     if rank == 0 and world == 1 and not args.no_ttt and args.config == "C2":

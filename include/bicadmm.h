@@ -76,6 +76,12 @@ typedef struct {
     int32_t block;      /* j in [0, M) */
     const void* A;      /* device pointer, see MEMORY above */
     int64_t lda;        /* row stride in elements, >= n_j, multiple of 4 */
+    void* ready_event;  /* optional cudaEvent_t (NULL = A and b_i already written): recorded by the
+                           caller after A_ij and the labels b_i were written on another stream.
+                           bicadmm_setup makes its stream wait on it right before the first read
+                           of this block (its Gram, a0), so host->device copies of later blocks
+                           overlap the factorisation of earlier ones; every such wait precedes the
+                           return of bicadmm_setup in stream order.  Not retained after setup. */
 } bicadmm_block;
 
 /* bicadmm_setup(A, b, loss, ...) of the north star: the data half. */

@@ -34,7 +34,7 @@ _i32, _i64, _f64, _vp = ct.c_int32, ct.c_int64, ct.c_double, ct.c_void_p
 
 
 class bicadmm_block(ct.Structure):
-    _fields_ = [("node", _i32), ("block", _i32), ("A", _vp), ("lda", _i64)]
+    _fields_ = [("node", _i32), ("block", _i32), ("A", _vp), ("lda", _i64), ("ready_event", _vp)]
 
 
 class bicadmm_problem(ct.Structure):
@@ -297,6 +297,7 @@ class BiCADMM:
         self.dtype = F64 if tdt == torch.float64 else F32
         self._keep = []
         blk = []
+        node_events = {}
         if blocks is None:
             for i, Ai in enumerate(A):
                 Ap, lda = _aligned_matrix(Ai, torch)
@@ -307,9 +308,16 @@ class BiCADMM:
             self.m = np.array([a.shape[0] for a in A], dtype=np.int64)
         else:
             ms = {}
-            for (i, j, Aij) in blocks:
+            for ent in blocks:
+                # (i, j, A_ij) or (i, j, A_ij, ready): ready a torch.cuda.Event recorded after A_ij
+                # and b_i were written (bicadmm_block.ready_event; setup waits on it per block)
+                i, j, Aij = ent[:3]
+                ev = ent[3] if len(ent) > 3 else None
                 assert Aij.stride(1) == 1
-                blk.append(bicadmm_block(i, j, Aij.data_ptr(), Aij.stride(0)))
+                if ev is not None:
+                    node_events.setdefault(i, []).append(ev)
+                blk.append(bicadmm_block(i, j, Aij.data_ptr(), Aij.stride(0),
+                                         ev.cuda_event if ev is not None else None))
                 ms[i] = Aij.shape[0]
                 self._keep.append(Aij)
             self.m = np.array([ms.get(i, b[i].shape[0] if b[i] is not None else 1) for i in range(self.N)],
@@ -322,6 +330,8 @@ class BiCADMM:
                 continue
             bi = b[i].contiguous()
             if check_domain:
+                for ev in node_events.get(i, ()):
+                    torch.cuda.current_stream(bi.device).wait_event(ev)
                 check_labels(self.loss, C, bi)
             self._keep.append(bi)
             bl.append(bi.data_ptr())

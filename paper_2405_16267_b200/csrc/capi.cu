@@ -80,6 +80,7 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     int node, block, user_index, li, jl;
     const void* A;
     int64_t lda, m, c0, nj;
+    void* ready = nullptr;   // caller's cudaEvent_t for A (setup only; bicadmm_block.ready_event)
     void* H;         // tall block: H = (rho_l A^T A + c I)^{-1} (nj x nj); fat block (Woodbury,
     int64_t ldh;     // m < nj): K^{-1} = ((c/rho_l) I + A A^T)^{-1} (m x m)
     bool fat = false;
@@ -345,6 +346,7 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         L.user_index = k;
         L.A = P->blocks[k].A;
         L.lda = P->blocks[k].lda;
+        L.ready = P->blocks[k].ready_event;
         L.m = P->m[L.node];
         L.c0 = P->col_start[L.block];
         L.nj = P->col_start[L.block + 1] - L.c0;
@@ -919,6 +921,10 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             LBlock& L = h->blk[b0 + k];
             const int64_t ldg = rup(L.kd, 8);
             double* G = h->gram + k * h->gram_stride;
+            if (L.ready && cudaStreamWaitEvent(h->st, (cudaEvent_t)L.ready, 0) != cudaSuccess) {
+                rc = BICADMM_ERR_CUDA;
+                break;
+            }
             if (L.fat)   // K = (c/rho_l) I + A A^T  (Woodbury, R27)
                 rc = launch_gram_rows(P->dtype, L.m, L.nj, L.A, L.lda, 1.0, c / R->rho_l, G, ldg, h->st);
             else if (h->gtc_ws)   // F = rho_l A^T A + c I  (Eq. (24)), tcgen05 Ozaki-scheme Gram
@@ -943,6 +949,7 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             return rc;
         }
     }
+    for (auto& L : h->blk) L.ready = nullptr;   // not retained (bicadmm_block.ready_event)
     cudaEventRecord(h->e1, h->st);
     if (cudaEventSynchronize(h->e1) != cudaSuccess) { bicadmm_destroy(h); return BICADMM_ERR_CUDA; }
     float ms = 0.f;

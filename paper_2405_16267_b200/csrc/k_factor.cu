@@ -30,6 +30,10 @@ struct GemmArgs {
     int lower_only;   // skip tiles strictly above the diagonal
     int mirror;       // also write the transpose into the upper triangle
     int tri_k;        // K range starts at max(m0, n0) (lower-triangular operands)
+    // Triangular operands whose zero half is skipped tile by tile (the skipped products are
+    // exact zeros, so the result is bit-identical to the full product):
+    int k_lo;         // 0: K from 0; 1: A(i,k) = 0 for k < i -> from m0; 2: B(k,j) = 0 for k < j -> from n0
+    int k_hi;         // 0: K to K; 1: A(i,k) = 0 for k > i -> to m0 + BM; 2: B(k,j) = 0 for k > j -> to n0 + BN
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -64,7 +68,11 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_dmma(const __grid_constan
 
     int64_t kb = 0;
     if (g.tri_k) kb = (m0 > n0 ? m0 : n0) / BK * BK;
-    const int64_t K = g.K;
+    if (g.k_lo == 1) kb = m0 / BK * BK;
+    if (g.k_lo == 2) kb = n0 / BK * BK;
+    int64_t K = g.K;
+    if (g.k_hi == 1 && m0 + BM < K) K = m0 + BM;
+    if (g.k_hi == 2 && n0 + BN < K) K = n0 + BN;
 
     double regA[8], regB[8];
     auto gload = [&](int64_t k0) {
@@ -314,7 +322,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.M = n2; g.N = n1; g.K = n1; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
         g.A = J[k].F + (off + n1) * J[k].ldf + off; g.lda = J[k].ldf;
         g.B = J[k].W + off * J[k].ldw + off; g.ldb = J[k].ldw;
-        g.C = J[k].X; g.ldc = J[k].ldw;
+        g.C = J[k].X; g.ldc = J[k].ldw; g.k_hi = 2;
         ga[k] = g;
     }
     rc = gemm_batched<double, double, true, true>(ga, nj, s);
@@ -341,7 +349,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.M = n2; g.N = n1; g.K = n1; g.alpha = 1.0; g.beta = 0.0; g.diag = 0.0;
         g.A = J[k].F + (off + n1) * J[k].ldf + off; g.lda = J[k].ldf;
         g.B = J[k].W + off * J[k].ldw + off; g.ldb = J[k].ldw;
-        g.C = J[k].X; g.ldc = J[k].ldw;
+        g.C = J[k].X; g.ldc = J[k].ldw; g.k_lo = 2;
         ga[k] = g;
     }
     rc = gemm_batched<double, double, true, false>(ga, nj, s);
@@ -352,7 +360,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.M = n2; g.N = n1; g.K = n2; g.alpha = -1.0; g.beta = 0.0; g.diag = 0.0;
         g.A = J[k].W + (off + n1) * J[k].ldw + off + n1; g.lda = J[k].ldw;
         g.B = J[k].X; g.ldb = J[k].ldw;
-        g.C = J[k].W + (off + n1) * J[k].ldw + off; g.ldc = J[k].ldw;
+        g.C = J[k].W + (off + n1) * J[k].ldw + off; g.ldc = J[k].ldw; g.k_hi = 1;
         ga[k] = g;
     }
     return gemm_batched<double, double, true, false>(ga, nj, s);

@@ -322,6 +322,41 @@ def test_graph_replay_bit_identical_to_eager(bc, sweep):
     assert out["1"][2] == out["0"][2]
 
 
+@pytest.mark.parametrize("M", [1, 2])
+def test_block_ready_events_order_setup_after_late_copies(bc, M):
+    # bicadmm_block.ready_event: node k's A and b are copied on another stream behind a ~0.1 s
+    # device sleep; setup must wait on each block's event before its Gram. Destinations start
+    # zeroed, so a Gram that ran early would factor c I and change every iterate.
+    P = dg.generate(3, 500, 96, 6, "logistic", seed=21)
+    cs = dg.block_partition(96, M)
+    prm = bc.Params(kappa=6, max_outer=6, inner_fixed=4, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", prm, cs)
+    s.iterate(5)
+    ref = (s.z, s.trace())
+    s.close()
+    hostA = [a.contiguous().pin_memory() for a in P.A]
+    hostb = [b.contiguous().pin_memory() for b in P.b]
+    dA = [torch.zeros_like(a, device="cuda") for a in P.A]
+    db = [torch.zeros_like(b, device="cuda") for b in P.b]
+    torch.cuda.synchronize()
+    cp = torch.cuda.Stream()
+    evs = []
+    with torch.cuda.stream(cp):
+        for k in range(3):
+            torch.cuda._sleep(50_000_000)
+            dA[k].copy_(hostA[k], non_blocking=True)
+            db[k].copy_(hostb[k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cp)
+            evs.append(ev)
+    blocks = [(k, j, dA[k][:, cs[j]:cs[j + 1]], evs[k]) for k in range(3) for j in range(M)]
+    s = bc.BiCADMM(None, db, "logistic", prm, cs, blocks=blocks)
+    s.iterate(5)
+    assert np.array_equal(s.z, ref[0])
+    assert np.array_equal(s.trace(), ref[1])
+    s.close()
+
+
 @pytest.mark.parametrize("groups", ["1", "2", "3", "4", "6"])
 def test_fused4_row_groups(bc, orc, groups):
     # the CTA-pair sweep with its 12 main warps split into row groups (partials per group);
