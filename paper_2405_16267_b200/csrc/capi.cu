@@ -68,6 +68,9 @@ NcclApi g_nccl;
 
 struct bicadmm_comm {
     int world = 1, rank = 0, device = 0, color = 0, group_size = 1;
+    // BICADMM_NCCL_SELF=1 with world == 1: a real one-rank NCCL communicator, so the
+    // multi-rank code path (collectives, split block sums, eager launches) runs on one GPU
+    bool self = false;
 #if BIC_HAVE_NCCL
     ncclComm_t world_comm = nullptr, group_comm = nullptr;
 #endif
@@ -749,11 +752,17 @@ int bicadmm_comm_init(int world, int rank, int device, const void* uid, int grou
     bicadmm_comm* c = new bicadmm_comm();
     c->world = world; c->rank = rank; c->device = device; c->color = group_color;
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return BICADMM_ERR_CUDA; }
-    if (world > 1) {
+    const char* se = getenv("BICADMM_NCCL_SELF");
+    c->self = world == 1 && se && atoi(se) != 0;
+    if (world > 1 || c->self) {
 #if BIC_HAVE_NCCL
-        if (!uid || !g_nccl.load()) { delete c; return BICADMM_ERR_NCCL; }
+        if ((!uid && !c->self) || !g_nccl.load()) { delete c; return BICADMM_ERR_NCCL; }
         ncclUniqueId id;
-        memcpy(&id, uid, sizeof(id));
+        if (c->self) {
+            if (g_nccl.GetUniqueId(&id) != ncclSuccess) { delete c; return BICADMM_ERR_NCCL; }
+        } else {
+            memcpy(&id, uid, sizeof(id));
+        }
         if (g_nccl.CommInitRank(&c->world_comm, world, id, rank) != ncclSuccess) { delete c; return BICADMM_ERR_NCCL; }
         if (g_nccl.CommSplit(c->world_comm, group_color, rank, &c->group_comm, nullptr) != ncclSuccess) {
             g_nccl.CommDestroy(c->world_comm);
@@ -798,17 +807,20 @@ int bicadmm_workspace_size(const bicadmm_problem* P, const bicadmm_params* R, si
 }  // extern "C"
 
 // ======================================================================= collectives
+// the handle runs the multi-rank path (NCCL collectives, no graphs)
+static bool multi_rank(const bicadmm_handle* h) { return h->comm && (h->comm->world > 1 || h->comm->self); }
+
 static int allreduce(bicadmm_handle* h, double* buf, int64_t count, bool group) {
 #if BIC_HAVE_NCCL
-    if (!h->comm || h->comm->world == 1 || count <= 0) return BICADMM_OK;
+    if (!multi_rank(h) || count <= 0) return BICADMM_OK;
     ncclComm_t c = group ? h->comm->group_comm : h->comm->world_comm;
-    if (group && h->comm->group_size == 1) return BICADMM_OK;
+    if (group && h->comm->group_size == 1 && !h->comm->self) return BICADMM_OK;
     if (g_nccl.AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, c, h->st) != ncclSuccess)
         return fail(h, BICADMM_ERR_NCCL, "ncclAllReduce");
     return BICADMM_OK;
 #else
     (void)buf; (void)count; (void)group;
-    return h->comm && h->comm->world > 1 ? fail(h, BICADMM_ERR_NCCL, "built without NCCL") : BICADMM_OK;
+    return multi_rank(h) ? fail(h, BICADMM_ERR_NCCL, "built without NCCL") : BICADMM_OK;
 #endif
 }
 
@@ -838,7 +850,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     if (((uintptr_t)ws) % 256) { delete h; return BICADMM_ERR_INVALID; }
     plan(h, P, ws);
     h->ws_bytes = ws_bytes;
-    if (comm && comm->world > 1) {
+    if (comm && comm->self) {
+        // one-rank NCCL test mode; BICADMM_NCCL_SELF=2 also routes every node's block sum
+        // through the per-sweep group AllReduce (the split-block path of block-major placements)
+        for (auto& nd : h->nod) if (nd.np != P->M) { delete h; return BICADMM_ERR_PLACEMENT; }
+        h->split_blocks = atoi(getenv("BICADMM_NCCL_SELF")) >= 2;
+    } else if (comm && comm->world > 1) {
         // a node whose M blocks are not all local has its block sum all-reduced per sweep
         for (auto& nd : h->nod) if (nd.np != P->M) h->split_blocks = true;
         if (h->split_blocks && comm->group_size * 1 < 2) { delete h; return BICADMM_ERR_PLACEMENT; }
@@ -1181,7 +1198,7 @@ static int outer_step(bicadmm_handle* h, bool readback = true) {
     H_RC(h, launch_s_update(h->len, h->prm.kappa, h->z, h->s, h->sc, h->st));
     H_RC(h, launch_u_update(h->bv.data(), (int)h->bv.size(), h->z, h->upart, h->st));
     H_RC(h, launch_node_sq(h->bv.data(), (int)h->bv.size(), h->upart, h->N, h->node_sq, h->st));
-    if (h->comm && h->comm->world > 1) {
+    if (multi_rank(h)) {
         // every (i, j) contributes exactly once: node_sq partials are per local block
         H_RC(h, allreduce(h, h->node_sq, h->N, false));
     }
@@ -1361,7 +1378,7 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
             // from the second outer iteration on, a fixed uniform schedule replays one CUDA graph
             // (single rank only: multi-rank runs keep the eager launches, NCCL outside graphs)
             const bool use_graph = graph_enabled() && !replay && uniform && k >= 1 && !h->graph.failed &&
-                                   !(h->comm && h->comm->world > 1);
+                                   !multi_rank(h);
             static const bool gdbg = getenv("BICADMM_GRAPH_DEBUG") != nullptr;
             if (gdbg) fprintf(stderr, "bicadmm: outer %d use_graph %d (replay %d uniform %d failed %d)\n", k, (int)use_graph,
                               (int)replay, (int)uniform, (int)h->graph.failed);
@@ -1648,7 +1665,7 @@ static int do_finalize(bicadmm_handle* h) {
     if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
     // logistic / softmax refit (DESIGN R29): single rank (the gathered support matrix is local)
     if (h->prm.refit && (h->loss == BICADMM_LOGISTIC || h->loss == BICADMM_SOFTMAX) && h->rf_AT &&
-        !(h->comm && h->comm->world > 1))
+        !multi_rank(h))
         H_RC(h, do_refit_newton(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
@@ -1683,7 +1700,7 @@ static int do_finalize(bicadmm_handle* h) {
     H_CUDA(h, cudaMemcpyAsync(nobj.data() + h->N, h->wsum, sizeof(double), cudaMemcpyDeviceToHost, h->st));
     H_CUDA(h, cudaStreamSynchronize(h->st));
     double obj = 0.0;
-    const double gs = (h->comm && h->comm->world > 1 && h->split_blocks) ? (double)h->comm->group_size : 1.0;
+    const double gs = (multi_rank(h) && h->split_blocks) ? (double)h->comm->group_size : 1.0;
     for (int i = 0; i < h->N; ++i) obj += nobj[i] / gs;
     obj += 0.5 * h->prm.lambda * nobj[h->N];
     h->objective = obj;
@@ -1731,7 +1748,7 @@ __global__ void k_loop_ctl(cudaGraphConditionalHandle hnd, const OuterScalars* _
 // budget), so the host waits once per launch instead of once per outer iteration.
 // Returns BICADMM_ERR_STATE when not applicable (the caller iterates from the host).
 static int solve_device_loop(bicadmm_handle* h) {
-    if (!graph_enabled() || h->prof || h->loop.failed || (h->comm && h->comm->world > 1) ||
+    if (!graph_enabled() || h->prof || h->loop.failed || multi_rank(h) ||
         h->prm.inner_fixed <= 0 || h->outer_done < 1 || h->converged)
         return BICADMM_ERR_STATE;
     if (!h->schedule.empty() && h->outer_done - h->sched_start < h->sched_rows) return BICADMM_ERR_STATE;

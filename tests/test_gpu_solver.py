@@ -465,3 +465,61 @@ def test_device_loop_solve_matches_host_loop(bc):
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
     assert a[5] == b[5]
     assert np.array_equal(a[6], b[6])
+
+
+SELF_CASES = [
+    # name, N, m_i, n, kappa, loss, M, C, refit
+    ("logistic_M1", 3, 700, 256, 8, "logistic", 1, 1, 0),
+    ("ls_M3_refit", 2, 500, 300, 10, "ls", 3, 1, 1),
+    ("softmax_M2", 2, 400, 120, 9, "softmax", 2, 4, 0),
+    ("hinge_M2", 2, 600, 200, 8, "hinge", 2, 1, 0),
+]
+
+
+@pytest.mark.parametrize("split", ["1", "2"], ids=["world_sums", "split_block_sums"])
+@pytest.mark.parametrize("case", SELF_CASES, ids=[c[0] for c in SELF_CASES])
+def test_nccl_one_rank_path_matches_local(bc, case, split):
+    # BICADMM_NCCL_SELF: a real one-rank NCCL communicator, so the multi-rank code path runs on one
+    # GPU -- eager launches (no graphs), the per-outer AllReduces of sum_i(x_i + u_i), the node
+    # residual partials and the objective; with "2" also the per-sweep group AllReduce of the
+    # node block sums S_i (Algorithm 2) that block-major placements use.  A one-rank
+    # AllReduce is a copy, so the iterates must equal the local (comm = None) run: bit for bit
+    # without split sums, and to 1e-13 with them (S_i is then summed by k_psum, not the prox kernel).
+    import os
+    name, N, m, n, kappa, loss, M, C, refit = case
+    P = dg.generate(N, m, n, kappa, loss, seed=31, C=C)
+    cs = dg.block_partition(n, M)
+    out = {}
+    for mode in ("local", "nccl"):
+        comm = None
+        if mode == "nccl":
+            os.environ["BICADMM_NCCL_SELF"] = split
+        try:
+            if mode == "nccl":
+                comm = bc.bicadmm_comm_init(1, 0, torch.cuda.current_device(), None, 0)
+            s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], loss,
+                           bc.Params(kappa=kappa, max_outer=40, inner_fixed=0, max_inner=20, eps_inner=1e-9,
+                                     eps_p=1e-7, eps_d=1e-7, eps_b=1e-7, refit=refit), cs, C=P.C, comm=comm)
+            s.iterate(3)
+            z3 = s.z
+            rep = s.solve()
+            rep = s.finalize()
+            out[mode] = dict(z3=z3, z=s.z, trace=s.trace(), obj=rep.objective, sup=s.support(),
+                             xf=s.get(bc.FIELD_X_FINAL), outer=rep.outer_iters, inner=rep.inner_sweeps)
+            s.close()
+        finally:
+            os.environ.pop("BICADMM_NCCL_SELF", None)
+            bc.bicadmm_comm_destroy(comm)
+    a, b = out["local"], out["nccl"]
+    if split == "1":
+        assert np.array_equal(a["z3"], b["z3"])
+        assert np.array_equal(a["z"], b["z"])
+        assert np.array_equal(a["trace"], b["trace"])
+        assert a["obj"] == b["obj"]
+    else:
+        assert _rel(b["z3"], a["z3"]) <= 1e-13
+        assert a["outer"] == b["outer"]
+        assert _rel(b["z"], a["z"]) <= 1e-11
+        assert abs(a["obj"] - b["obj"]) <= 1e-11 * abs(a["obj"])
+    assert np.array_equal(a["sup"], b["sup"])
+    assert _rel(b["xf"], a["xf"]) <= 1e-11
