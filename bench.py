@@ -204,6 +204,8 @@ def run_ours(args):
         uid = [bc.bicadmm_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = bc.bicadmm_comm_init(world, rank, local, uid[0], rank)  # node-major: own group
+    elif os.environ.get("BICADMM_NCCL_SELF"):   # one-rank NCCL communicator: the multi-rank code path
+        comm = bc.bicadmm_comm_init(1, 0, local, None, 0)
     b_all = [None] * N
     blocks = []
     for k in range(nl):
