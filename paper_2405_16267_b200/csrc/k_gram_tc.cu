@@ -2,25 +2,32 @@
 // (Ozaki-scheme emulation on tcgen05 kind::i8).
 //
 // sm_100a has no FP64 tcgen05 kind; the FP64 DMMA path (k_factor.cu) runs near its
-// ~40 TFLOP/s peak.  Here every column l of A is scaled by 2^-e_l (|A[:,l]| < 2^e_l) and
-// split exactly into S signed 7-bit slices,
-//     A[r,l] 2^-e_l = sum_{s=1..S} d_s[r,l] 2^-7s + eps,   d_s in [-127, 127], |eps| < 2^-7S
-// (S = 8: 56 bits below the column maximum, for FP64 and FP32 data alike), so that
-//     G[i,j] = 2^(e_i+e_j) sum_{s+t <= S+1} 2^-7(s+t) (D_s^T D_t)[i,j]     (+ O(2^-7(S+1)))
+// ~40 TFLOP/s peak.  Here every column l of A is scaled by 2^-e_l (|A[:,l]| 128 < 127 2^e_l)
+// and split into S balanced digits by round-to-nearest,
+//     A[r,l] 2^-e_l = sum_{s=1..S} d_s[r,l] 2^-7s + eps,  d_1 in [-127, 127], d_s in [-64, 64],
+//     |eps| <= 2^-(7S+1)
+// (S = 7: 50 bits below the column maximum, for FP64 and FP32 data alike), so that
+//     G[i,j] = 2^(e_i+e_j) sum_{s+t <= S+1} 2^-7(s+t) (D_s^T D_t)[i,j]     (+ dropped terms)
+// Round-to-nearest digits carry no sign bias (truncated digits all share the sign of the
+// entry, so the dropped products of a diagonal entry G_ii would add up coherently: that
+// costs ~1e-13 at S = 7); the dropped terms (s + t >= S + 2) and eps are zero-mean.
 // Each D_s^T D_t is an exact int8 x int8 -> int32 product on tcgen05.mma kind::i8; the
-// products of equal weight w = s + t accumulate in one TMEM accumulator (8 accumulators of
-// 128 x 64 int32 = all 512 TMEM columns), flushed to FP64 registers every 16,384 rows
-// (int32 headroom: 8 products x 127^2 x 16,384 < 2^31).  The weighted sum over w is formed
+// products of equal weight w = s + t accumulate in one TMEM accumulator (7 accumulators of
+// 128 x 64 int32 = TMEM columns 0..447), flushed to FP64 registers every 16,384 rows
+// (int32 headroom: 7 products x 127^2 x 16,384 < 2^31).  The weighted sum over w is formed
 // in FP64 in a fixed order (deterministic), scaled, and written as alpha G + diag I (lower
-// triangle).  Error per entry ~2^-56 m max|A_i| max|A_j| (FP64 data).
+// triangle).  Measured error <= ~2e-14 of sqrt(G_ii G_jj) (tests/test_gpu_ops.py).
+// (A-in-TMEM operands were measured and rejected: tools/tc_i8_rate.cu -- at N = 64 a
+// tcgen05.mma takes ~45 cycles with A in TMEM vs 48 from shared memory, and the
+// tcgen05.cp + slot-reuse waits cost more than that saves.)
 //
 // Pipeline per CTA (one 128 x 64 tile of G, lower triangle of tiles):
 //   warp 5    : one thread issues the TMA copies (cp.async.bulk.tensor.2d, SWIZZLE_32B) of
-//               the S slices of 32 rows x (128 + 64) columns into a 4-stage ring
+//               the S slices of 32 rows x (128 + 64) columns into a 5-stage ring
 //   warp 4    : one thread issues S(S+1)/2 tcgen05.mma (M 128, N 64, K 32) per stage,
 //               commits to the stage's "empty" barrier and, per 16,384-row round, to
 //               "acc_full"
-//   warps 0-3 : the TMEM epilogue (tcgen05.ld of the 8 accumulators per round)
+//   warps 0-3 : the TMEM epilogue (tcgen05.ld of the 7 accumulators per round)
 // The slices are produced once per block by k_oz_split (column-major int8, zero padded).
 #include <cuda.h>
 #include <stdint.h>
@@ -32,14 +39,16 @@
 namespace bic {
 
 constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 32;   // tile M (columns i), N (columns j), K (rows per stage)
-constexpr int kOzSMax = 8;
-constexpr int kOzStages = 4;
+constexpr int kOzSMax = 7;                            // digits S; weights 2 .. S + 1
+constexpr int kOzStages = 5;
 constexpr int kOzRoundStages = 16384 / kOzBK;         // stages per int32 accumulation round
 constexpr int kOzThreads = 192;                       // 4 epilogue warps, 1 MMA warp, 1 TMA warp
-constexpr size_t kOzStageBytes = (size_t)kOzSMax * (kOzBM + kOzBN) * kOzBK;   // 48 KB
+constexpr size_t kOzStageBytes = (size_t)kOzSMax * (kOzBM + kOzBN) * kOzBK;   // 42 KB
 constexpr int kOzRowChunk = 32768;                    // rows of A split per launch pair
 
 __device__ __forceinline__ uint32_t oz_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// column exponent: 128 |A[:,l]| 2^-e < 127, so the first round-to-nearest digit fits int8
+__device__ __forceinline__ int oz_exp(double mx) { return mx > 0.0 ? ilogb(mx * (128.0 / 127.0)) + 1 : 0; }
 
 // ----------------------------------------------------------------------------- exponents
 // colmax[l] = max_r |A[r,l]| as order-preserving int64 bits (atomicMax: exact, deterministic)
@@ -64,11 +73,7 @@ __global__ void k_oz_split(const T* __restrict__ A, int64_t lda, int64_t m, int6
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t rg = (int64_t)blockIdx.y * 32;   // row group within this chunk
     if (l >= np || rg >= mp) return;
-    int e = 0;
-    if (l < n) {
-        const double mx = __longlong_as_double((long long)colmax[l]);
-        e = mx > 0.0 ? ilogb(mx) + 1 : 0;           // |A[:, l]| < 2^e
-    }
+    const int e = l < n ? oz_exp(__longlong_as_double((long long)colmax[l])) : 0;
     uint32_t pk[kOzSMax][8];
 #pragma unroll
     for (int s = 0; s < kOzSMax; ++s)
@@ -83,8 +88,8 @@ __global__ void k_oz_split(const T* __restrict__ A, int64_t lda, int64_t m, int6
         for (int s = 0; s < kOzSMax; ++s) {
             if (s < S) {
                 const double t = a * 128.0;               // exact
-                const double d = trunc(t);                // |d| <= 127
-                a = t - d;                                // exact
+                const double d = rint(t);                 // |d| <= 127 (s = 1), <= 64 (s > 1)
+                a = t - d;                                // exact, |a| <= 1/2
                 const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
                 pk[s][k >> 2] |= byte << (8 * (k & 3));
             }
@@ -288,15 +293,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         // write alpha 2^(e_i + e_j) acc (+ diag on i == j), lower triangle
         const int64_t i = i0 + 32 * warp + lane;
         if (i < a.n) {
-            const double mi = __longlong_as_double((long long)a.colmax[i]);
-            const int ei = mi > 0.0 ? ilogb(mi) + 1 : 0;
+            const int ei = oz_exp(__longlong_as_double((long long)a.colmax[i]));
             double* grow = a.G + i * a.ldg;
 #pragma unroll 4
             for (int c = 0; c < kOzBN; ++c) {
                 const int64_t j = j0 + c;
                 if (j > i || j >= a.n) continue;
-                const double mj = __longlong_as_double((long long)a.colmax[j]);
-                const int ej = mj > 0.0 ? ilogb(mj) + 1 : 0;
+                const int ej = oz_exp(__longlong_as_double((long long)a.colmax[j]));
                 double v = a.alpha * ldexp(acc[c], ei + ej);
                 if (a.accumulate) v += grow[j];
                 else if (i == j) v += a.diag;

@@ -166,7 +166,7 @@ def test_gram_tc(bc, m, nj, dt):
     lo = np.tril_indices(nj)
     d = np.sqrt(np.abs(np.diag(ref)))
     err = np.abs(Gn - ref)[lo] / np.outer(d, d)[lo]     # relative to sqrt(G_ii G_jj)
-    assert np.max(err) <= 1e-13
+    assert np.max(err) <= 3e-14   # S = 7 round-to-nearest digits: measured <= 5e-15
     assert np.all(Gn[np.triu_indices(nj, 1)] == 7.0)     # upper triangle untouched
 
 
