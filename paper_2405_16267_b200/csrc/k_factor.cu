@@ -208,7 +208,7 @@ int launch_gram_rows(int dtype, int64_t m, int64_t nj, const void* A, int64_t ld
 // ------------------------------------------------------------------ Cholesky diag block
 // One CTA factors the kn x kn diagonal block (kn <= 64) of F in place (lower, upper
 // zeroed) and writes W_kk = L_kk^{-1} (lower) into Wd.  Unblocked right-looking
-// Cholesky in shared memory, then column-parallel forward substitution.
+// Cholesky in shared memory with the inverse formed by the same elimination steps.
 constexpr int NB = 64;
 constexpr int kDiagThreads = 256;
 
@@ -233,40 +233,41 @@ __global__ void __launch_bounds__(kDiagThreads) k_chol_diag(const __grid_constan
     for (int e = tid; e < kn * kn; e += kDiagThreads) {
         const int i = e / kn, j = e % kn;
         L[i][j] = j <= i ? F[i * ldf + j] : 0.0;
-        W[i][j] = 0.0;
+        W[i][j] = i == j ? 1.0 : 0.0;
     }
     __syncthreads();
+    // Right-looking Cholesky with the inverse built alongside by the same row operations
+    // on [L | I] (forward elimination): step j scales column j of L and row j of W by
+    // 1/sqrt(d_j), then subtracts L[i][j] x (row j) from rows i > j of both.  Two barriers
+    // per column; 16 x 16 thread grid over the update regions.
+    const int tx = tid & 15, ty = tid >> 4;
     for (int j = 0; j < kn; ++j) {
-        if (tid == 0) {
-            const double d = L[j][j];
-            if (!(d > 0.0)) { atomicExch(info, 1); L[j][j] = 1.0; }
-            else L[j][j] = sqrt(d);
+        double d = L[j][j];
+        if (!(d > 0.0)) {
+            if (tid == 0) atomicExch(info, 1);
+            d = 1.0;
+        }
+        const double rl = 1.0 / sqrt(d);
+        __syncthreads();   // every thread has read the pivot before it is overwritten
+        if (tid < 64) {
+            const int i = j + tid;
+            if (i < kn) L[i][j] = i == j ? sqrt(d) : L[i][j] * rl;
+        } else if (tid < 128) {
+            const int c = tid - 64;
+            if (c <= j) W[j][c] *= rl;
         }
         __syncthreads();
-        const double ljj = L[j][j];
-        for (int i = j + 1 + tid; i < kn; i += kDiagThreads) L[i][j] /= ljj;
-        __syncthreads();
-        const int rem = kn - j - 1;
-        for (int e = tid; e < rem * rem; e += kDiagThreads) {
-            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+        for (int i = j + 1 + ty; i < kn; i += 16) {
+            const double lij = L[i][j];
+            for (int k = j + 1 + tx; k <= i; k += 16) L[i][k] -= lij * L[k][j];
+            for (int c = tx; c <= j; c += 16) W[i][c] -= lij * W[j][c];
         }
         __syncthreads();
     }
-    if (tid < kn) {
-        const int c = tid;
-        W[c][c] = 1.0 / L[c][c];
-        for (int i = c + 1; i < kn; ++i) {
-            double s = 0.0;
-            for (int k = c; k < i; ++k) s += L[i][k] * W[k][c];
-            W[i][c] = -s / L[i][i];
-        }
-    }
-    __syncthreads();
     for (int e = tid; e < kn * kn; e += kDiagThreads) {
         const int i = e / kn, j = e % kn;
         F[i * ldf + j] = j <= i ? L[i][j] : 0.0;
-        Wd[i * ldw + j] = W[i][j];
+        Wd[i * ldw + j] = j <= i ? W[i][j] : 0.0;
     }
 }
 
