@@ -47,14 +47,31 @@ int bicadmm_op_gram(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda
                     double alpha, double diag, double* G, int64_t ldg, void* stream);
 
 /* The same Gram on the 5th-generation tensor cores: FP64-accurate
- * Ozaki-scheme emulation with exact int8 slices of the column-scaled A on tcgen05.mma
- * kind::i8 (S = 8 slices: 56 bits below each column's maximum), TMEM accumulators, FP64 recombination.
+ * Ozaki-scheme emulation with int8 digits of the column-scaled A on tcgen05.mma kind::i8
+ * (S = 7 round-to-nearest digits: 50 bits below each column's maximum), TMEM int32
+ * accumulators, FP64 recombination.
  * Writes the LOWER triangle of G = alpha A^T A + diag I (FP64, ldg >= nj); the upper triangle
  * is left untouched.  ws: device scratch >= bicadmm_op_gram_tc_ws(dtype, m, nj) bytes
  * (caller-owned).  Errors: BICADMM_ERR_INVALID on bad sizes or a short workspace. */
 size_t bicadmm_op_gram_tc_ws(int dtype, int64_t m, int64_t nj);
 int bicadmm_op_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag,
                        double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream);
+
+/* General product on the same tcgen05 Ozaki engine (used by the a0 factor for its large
+ * GEMMs): C = alpha A_op B_op + beta C (+ diag on i == j), C FP64 row-major (ldc),
+ *   A_op(i, k) = A[i a_sl + k a_sr]  (M x K),   B_op(k, j) = B[j b_sl + k b_sr]  (K x N),
+ * A and B of the storage type dtype (device, caller-owned); rows of A_op and columns of B_op
+ * are scaled by their own power of two.  flags: bit 0 lower (M == N; only entries j <= i
+ * written), bit 1 mirror (also C[j][i]), bits 4-5 k_lo, bits 8-9 k_hi: operand zero
+ * structure whose tiles are skipped exactly -- k_lo 1: A_op(i,k) = 0 for k < i, 2: B_op(k,j) = 0
+ * for k < j, 3: zero unless k >= max(i, j); k_hi 1: A_op(i,k) = 0 for k > i, 2: B_op(k,j) = 0
+ * for k > j.  same != 0: B_op = A_op^T (B, b_sl, b_sr ignored; one digit set).
+ * ws: device scratch >= bicadmm_op_gemm_tc_ws(M, N, K, same) bytes.
+ * Errors: BICADMM_ERR_INVALID on bad sizes / flags or a short workspace. */
+size_t bicadmm_op_gemm_tc_ws(int64_t M, int64_t N, int64_t K, int same);
+int bicadmm_op_gemm_tc(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t a_sl, int64_t a_sr,
+                       const void* B, int64_t b_sl, int64_t b_sr, int same, double alpha, double beta, double diag,
+                       double* C, int64_t ldc, int flags, void* ws, size_t ws_bytes, void* stream);
 
 /* a10 ((7b); DESIGN R3): wbar = wsum / N; exact (z,t) minimiser by the
  * weighted soft-threshold with tau the root of N rho_c tau = rho_b (psi(tau) - v).

@@ -67,7 +67,8 @@ ABI_SYMBOLS = [
     "bicadmm_finalize", "bicadmm_set_schedule", "bicadmm_get", "bicadmm_last_error", "bicadmm_destroy",
     "bicadmm_set_profiling",
     "bicadmm_op_gemv", "bicadmm_op_gemv_t_ws", "bicadmm_op_gemv_t", "bicadmm_op_prox", "bicadmm_op_block_factor_ws",
-    "bicadmm_op_block_factor", "bicadmm_op_gram", "bicadmm_op_gram_tc_ws", "bicadmm_op_gram_tc", "bicadmm_op_zt", "bicadmm_op_s_update", "bicadmm_op_support",
+    "bicadmm_op_block_factor", "bicadmm_op_gram", "bicadmm_op_gram_tc_ws", "bicadmm_op_gram_tc",
+    "bicadmm_op_gemm_tc_ws", "bicadmm_op_gemm_tc", "bicadmm_op_zt", "bicadmm_op_s_update", "bicadmm_op_support",
     "bicadmm_launch_count",
 ]
 
@@ -124,6 +125,9 @@ def lib() -> ct.CDLL:
                                                ct.c_size_t, _vp]),
         "bicadmm_op_gram": (ct.c_int, [ct.c_int, _i64, _i64, _vp, _i64, _f64, _f64, _vp, _i64, _vp]),
         "bicadmm_op_gram_tc_ws": (ct.c_size_t, [ct.c_int, _i64, _i64]),
+        "bicadmm_op_gemm_tc_ws": (ct.c_size_t, [_i64, _i64, _i64, ct.c_int]),
+        "bicadmm_op_gemm_tc": (ct.c_int, [ct.c_int, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _i64, ct.c_int,
+                                          _f64, _f64, _f64, _vp, _i64, ct.c_int, _vp, ct.c_size_t, _vp]),
         "bicadmm_op_gram_tc": (ct.c_int, [ct.c_int, _i64, _i64, _vp, _i64, _f64, _f64, _vp, _i64, _vp, ct.c_size_t, _vp]),
         "bicadmm_op_zt": (ct.c_int, [_i64, ct.c_int, _f64, _f64, _vp, _vp, _f64, _vp, _vp, _vp, P(_f64), _vp]),
         "bicadmm_op_s_update": (ct.c_int, [_i64, _i64, _vp, _f64, _f64, _vp, P(_f64), _vp]),

@@ -51,29 +51,31 @@ __device__ __forceinline__ uint32_t oz_smem(const void* p) { return (uint32_t)__
 __device__ __forceinline__ int oz_exp(double mx) { return mx > 0.0 ? ilogb(mx * (128.0 / 127.0)) + 1 : 0; }
 
 // ----------------------------------------------------------------------------- exponents
-// colmax[l] = max_r |A[r,l]| as order-preserving int64 bits (atomicMax: exact, deterministic)
+// Operand element (l, r) = src[l * sl + r * sr]: l indexes the MMA operand rows (columns of
+// A for a Gram, rows of the left factor, columns of the right factor), r the summed index.
+// mx[l] = max_r |(l, r)| as order-preserving int64 bits (atomicMax: exact, deterministic)
 template <typename T>
-__global__ void k_oz_colmax(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t rows_per,
-                            unsigned long long* __restrict__ colmax) {
+__global__ void k_oz_absmax(const T* __restrict__ src, int64_t sl, int64_t sr, int64_t L, int64_t R,
+                            int64_t r_per, unsigned long long* __restrict__ mx) {
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= n) return;
-    const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
-    double mx = 0.0;
-    for (int64_t r = r0; r < r1; ++r) mx = fmax(mx, fabs((double)A[r * lda + l]));
-    atomicMax(colmax + l, (unsigned long long)__double_as_longlong(mx));
+    if (l >= L) return;
+    const int64_t r0 = (int64_t)blockIdx.y * r_per, r1 = r0 + r_per < R ? r0 + r_per : R;
+    double m = 0.0;
+    for (int64_t r = r0; r < r1; ++r) m = fmax(m, fabs((double)src[l * sl + r * sr]));
+    atomicMax(mx + l, (unsigned long long)__double_as_longlong(m));
 }
 
 // ----------------------------------------------------------------------------- split
-// Thread = (column l, 32 rows): slices written as out[s][l][r] (column-major, row stride
-// mp), 32 bytes per slice per thread.  Rows >= m and columns >= n are zero.
+// Thread = (operand row l, 32 summed indices): digits written as out[s][l][r] (K-major,
+// row stride Kp), 32 bytes per digit per thread.  r >= rows and l >= L are zero.
 template <typename T>
-__global__ void k_oz_split(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t r_begin,
-                           int64_t rows, const unsigned long long* __restrict__ colmax, int S, int8_t* __restrict__ out,
-                           int64_t np, int64_t mp) {
+__global__ void k_oz_split(const T* __restrict__ src, int64_t sl, int64_t sr, int64_t L, int64_t r_begin,
+                           int64_t rows, const unsigned long long* __restrict__ mx, int8_t* __restrict__ out,
+                           int64_t Lp, int64_t Kp) {
     const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t rg = (int64_t)blockIdx.y * 32;   // row group within this chunk
-    if (l >= np || rg >= mp) return;
-    const int e = l < n ? oz_exp(__longlong_as_double((long long)colmax[l])) : 0;
+    const int64_t rg = (int64_t)blockIdx.y * 32;   // summed-index group within this chunk
+    if (l >= Lp || rg >= Kp) return;
+    const int e = l < L ? oz_exp(__longlong_as_double((long long)mx[l])) : 0;
     uint32_t pk[kOzSMax][8];
 #pragma unroll
     for (int s = 0; s < kOzSMax; ++s)
@@ -83,22 +85,19 @@ __global__ void k_oz_split(const T* __restrict__ A, int64_t lda, int64_t m, int6
     for (int k = 0; k < 32; ++k) {
         const int64_t r = rg + k;
         double a = 0.0;
-        if (l < n && r < rows && r_begin + r < m) a = scalbn((double)A[(r_begin + r) * lda + l], -e);
+        if (l < L && r < rows) a = scalbn((double)src[l * sl + (r_begin + r) * sr], -e);
 #pragma unroll
         for (int s = 0; s < kOzSMax; ++s) {
-            if (s < S) {
-                const double t = a * 128.0;               // exact
-                const double d = rint(t);                 // |d| <= 127 (s = 1), <= 64 (s > 1)
-                a = t - d;                                // exact, |a| <= 1/2
-                const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
-                pk[s][k >> 2] |= byte << (8 * (k & 3));
-            }
+            const double t = a * 128.0;               // exact
+            const double d = rint(t);                 // |d| <= 127 (s = 1), <= 64 (s > 1)
+            a = t - d;                                // exact, |a| <= 1/2
+            const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
+            pk[s][k >> 2] |= byte << (8 * (k & 3));
         }
     }
 #pragma unroll
     for (int s = 0; s < kOzSMax; ++s) {
-        if (s >= S) break;
-        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * np + l) * mp + rg);
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * Lp + l) * Kp + rg);
         dst[0] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
         dst[1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
     }
@@ -156,31 +155,52 @@ __device__ __forceinline__ void oz_ld64(uint32_t taddr, uint32_t (&v)[64]) {
 }
 
 struct OzArgs {
-    int64_t np, mp, n;       // padded columns, padded rows of this chunk, true columns
-    const unsigned long long* colmax;
-    int S;
-    double alpha, diag;
-    double* G;
-    int64_t ldg;
-    int accumulate;          // add into G (row chunks after the first); else overwrite
+    int64_t M, N;            // true sizes of C (rows i: A-operand rows; columns j: B-operand rows)
+    int64_t Mp, Np, Kp;      // padded A / B operand rows, padded summed index of this chunk
+    int64_t ntj;             // column tiles (rectangular tile set)
+    int lower;               // tiles meeting the lower triangle only (M == N); entries j <= i
+    int mirror;              // also write C[j][i] for the written i > j
+    int k_lo, k_hi;          // zero structure of the operands (launch_gemm_tc), absolute indices
+    int64_t K, r_begin;      // total summed length; this chunk starts at r_begin
+    const unsigned long long *amax, *bmax;   // per-row maxima of the A / B operands
+    double alpha, beta, diag;
+    double* C;
+    int64_t ldc;
 };
 
+// One 128 x 64 tile of C = alpha A B^T-ish (both operands K-major digit slices) + beta C + diag I
 __global__ void __launch_bounds__(kOzThreads, 1)
-    k_oz_gram(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ OzArgs a) {
+    k_oz_mm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ OzArgs a) {
     extern __shared__ __align__(1024) uint8_t oz_sm_raw[];
     uint8_t* oz_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_sm_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[kOzStages], empty[kOzStages], acc_full, acc_empty;
     __shared__ uint32_t tmem_base;
-    // tile (bi, bj): column block bi of 128 (rows of G), bj of 64 with 64 bj < 128 (bi + 1)
-    int64_t t = blockIdx.x, bi = 0;
-    while (t >= 2 * bi + 2) { t -= 2 * bi + 2; ++bi; }
-    const int64_t bj = t;
+    int64_t bi, bj;
+    if (a.lower) {   // column block bi of 128 (rows of C), bj of 64 with 64 bj < 128 (bi + 1)
+        int64_t t = blockIdx.x;
+        bi = 0;
+        while (t >= 2 * bi + 2) { t -= 2 * bi + 2; ++bi; }
+        bj = t;
+    } else {
+        bi = (int64_t)blockIdx.x / a.ntj;
+        bj = (int64_t)blockIdx.x % a.ntj;
+    }
     const int64_t i0 = bi * kOzBM, j0 = bj * kOzBN;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int S = a.S;
-    const int nstage = (int)(a.mp / kOzBK);
-    const uint32_t bytes_stage = (uint32_t)(S * (kOzBM + kOzBN) * kOzBK);
+    // summed range of this tile (structural zeros skipped), relative to the chunk, in stages
+    int64_t klo = 0, khi = a.K;
+    if (a.k_lo == 1) klo = i0;
+    if (a.k_lo == 2) klo = j0;
+    if (a.k_lo == 3) klo = i0 > j0 ? i0 : j0;
+    if (a.k_hi == 1 && i0 + kOzBM < khi) khi = i0 + kOzBM;
+    if (a.k_hi == 2 && j0 + kOzBN < khi) khi = j0 + kOzBN;
+    klo = (klo > a.r_begin ? klo : a.r_begin) - a.r_begin;
+    khi = (khi < a.r_begin + a.Kp ? khi : a.r_begin + a.Kp) - a.r_begin;
+    const int st0 = (int)(klo / kOzBK);
+    const int st1 = khi > klo ? (int)((khi + kOzBK - 1) / kOzBK) : st0;
+    const int nstage = st1 - st0;
+    const uint32_t bytes_stage = (uint32_t)(kOzSMax * (kOzBM + kOzBN) * kOzBK);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_smem(&tmem_base)),
                      "r"(512));
@@ -204,16 +224,16 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (warp == 5) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            for (int st = 0; st < nstage; ++st) {
-                const int sb = st % kOzStages;
-                if (st >= kOzStages) oz_mbar_wait(&empty[sb], (uint32_t)((st / kOzStages - 1) & 1));
+            for (int q = 0; q < nstage; ++q) {
+                const int sb = q % kOzStages;
+                if (q >= kOzStages) oz_mbar_wait(&empty[sb], (uint32_t)((q / kOzStages - 1) & 1));
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_smem(&full[sb])),
                              "r"(bytes_stage) : "memory");
                 uint8_t* base = oz_sm + (size_t)sb * kOzStageBytes;
-                const int k0 = st * kOzBK;
+                const int k0 = (st0 + q) * kOzBK;
 #pragma unroll
                 for (int s = 0; s < kOzSMax; ++s) {
-                    const int ra = (int)(s * a.np + i0), rbb = (int)(s * a.np + j0);   // S == kOzSMax
+                    const int ra = (int)(s * a.Mp + i0), rbb = (int)(s * a.Np + j0);
                     asm volatile(
                         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                         ::"r"(oz_smem(base + (size_t)s * kOzBM * kOzBK)), "l"(&tmA), "r"(k0), "r"(ra),
@@ -232,21 +252,21 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) |
                                    ((uint32_t)(kOzBM >> 4) << 24);
             const uint32_t smem0 = oz_smem(oz_sm);
-            int st = 0;
+            int q = 0;
             for (int rd = 0; rd < nround; ++rd) {
                 if (rd > 0) oz_mbar_wait(&acc_empty, (uint32_t)((rd - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const int st_end = (rd + 1) * kOzRoundStages < nstage ? (rd + 1) * kOzRoundStages : nstage;
-                const int st_begin = st;
-                for (; st < st_end; ++st) {
-                    const int sb = st % kOzStages;
-                    oz_mbar_wait(&full[sb], (uint32_t)((st / kOzStages) & 1));
+                const int q_end = (rd + 1) * kOzRoundStages < nstage ? (rd + 1) * kOzRoundStages : nstage;
+                const int q_begin = q;
+                for (; q < q_end; ++q) {
+                    const int sb = q % kOzStages;
+                    oz_mbar_wait(&full[sb], (uint32_t)((q / kOzStages) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     // descriptors: the start-address field is bits [0,14) in 16-byte units, so the
                     // slice tiles of this stage are fixed offsets from the stage's base descriptor
                     const uint64_t dA0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes));
                     const uint64_t dB0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes) + (uint32_t)(kOzSMax * kOzBM * kOzBK));
-                    const uint32_t first = st == st_begin ? 1u : 0u;
+                    const uint32_t first = q == q_begin ? 1u : 0u;
 #pragma unroll
                     for (int sa = 1; sa <= kOzSMax; ++sa)
 #pragma unroll
@@ -279,7 +299,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             oz_mbar_wait_sleep(&acc_full, (uint32_t)(rd & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
-            for (int w = 2; w <= S + 1; ++w) {   // fixed order w = 2 .. S + 1
+            for (int w = 2; w <= kOzSMax + 1; ++w) {   // fixed order w = 2 .. S + 1
                 uint32_t v[64];
                 oz_ld64(lane_addr + (uint32_t)((w - 2) * kOzBN), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -290,20 +310,21 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             oz_mbar_arrive(&acc_empty);
         }
-        // write alpha 2^(e_i + e_j) acc (+ diag on i == j), lower triangle
+        // C[i][j] = alpha 2^(e_i + f_j) acc + beta C[i][j] (+ diag on i == j)
         const int64_t i = i0 + 32 * warp + lane;
-        if (i < a.n) {
-            const int ei = oz_exp(__longlong_as_double((long long)a.colmax[i]));
-            double* grow = a.G + i * a.ldg;
+        if (i < a.M) {
+            const int ei = oz_exp(__longlong_as_double((long long)a.amax[i]));
+            double* crow = a.C + i * a.ldc;
 #pragma unroll 4
             for (int c = 0; c < kOzBN; ++c) {
                 const int64_t j = j0 + c;
-                if (j > i || j >= a.n) continue;
-                const int ej = oz_exp(__longlong_as_double((long long)a.colmax[j]));
+                if (j >= a.N || (a.lower && j > i)) continue;
+                const int ej = oz_exp(__longlong_as_double((long long)a.bmax[j]));
                 double v = a.alpha * ldexp(acc[c], ei + ej);
-                if (a.accumulate) v += grow[j];
-                else if (i == j) v += a.diag;
-                grow[j] = v;
+                if (a.beta != 0.0) v += a.beta * crow[j];
+                if (i == j) v += a.diag;
+                crow[j] = v;
+                if (a.mirror && j < i) a.C[j * a.ldc + i] = v;
             }
         }
     }
@@ -315,12 +336,18 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 // ----------------------------------------------------------------------------- host
 static int64_t oz_rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// scratch: A digits [S][Mp][Kp] (+ B digits [S][Np][Kp] unless B is A) + row maxima
+size_t gemm_tc_scratch_bytes(int64_t M, int64_t N, int64_t K, bool same) {
+    const int64_t Mp = oz_rup(M, kOzBM), Np = oz_rup(N, kOzBM);
+    const int64_t Kp = oz_rup(K < kOzRowChunk ? K : kOzRowChunk, kOzBK);
+    size_t b = (size_t)oz_rup((int64_t)kOzSMax * Mp * Kp, 256);
+    if (!same) b += (size_t)oz_rup((int64_t)kOzSMax * Np * Kp, 256);
+    return b + sizeof(unsigned long long) * (size_t)(Mp + (same ? 0 : Np)) + 1024;
+}
+
 size_t gram_tc_scratch_bytes(int dtype, int64_t m, int64_t nj) {
     (void)dtype;
-    const int S = kOzSMax;
-    const int64_t np = oz_rup(nj, kOzBM), rows = m < kOzRowChunk ? m : kOzRowChunk;
-    const int64_t mp = oz_rup(rows, kOzBK);
-    return (size_t)S * np * mp + sizeof(unsigned long long) * (size_t)np + 1024;
+    return gemm_tc_scratch_bytes(nj, nj, m, true);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -339,13 +366,13 @@ static EncodeTiledFn oz_encode() {
     return fn;
 }
 
-// 2-D map over the slices [S * np rows (slice, column)] x [mp bytes (rows of A)], box
+// 2-D map over digits [S * Lp rows (digit, operand row)] x [Kp bytes (summed index)], box
 // {32 bytes, box_rows}, 32-byte swizzle (the UMMA K-major SWIZZLE_32B layout)
-static int oz_map(CUtensorMap* map, int8_t* sl, int64_t S, int64_t np, int64_t mp, uint32_t box_rows) {
+static int oz_map(CUtensorMap* map, int8_t* sl, int64_t Lp, int64_t Kp, uint32_t box_rows) {
     EncodeTiledFn enc = oz_encode();
     if (!enc) return BICADMM_ERR_CUDA;
-    const cuuint64_t dims[2] = {(cuuint64_t)mp, (cuuint64_t)(S * np)};
-    const cuuint64_t strides[1] = {(cuuint64_t)mp};
+    const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)(kOzSMax * Lp)};
+    const cuuint64_t strides[1] = {(cuuint64_t)Kp};
     const cuuint32_t box[2] = {(cuuint32_t)kOzBK, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, sl, dims, strides, box, estr,
@@ -359,54 +386,97 @@ bool gram_tc_enabled() {
     return on;
 }
 
-int launch_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag, double* G,
-                   int64_t ldg, void* scratch, size_t scratch_bytes, cudaStream_t s) {
-    if (m <= 0 || nj <= 0) return BICADMM_OK;
-    if (scratch_bytes < gram_tc_scratch_bytes(dtype, m, nj)) return BICADMM_ERR_INVALID;
-    const int S = kOzSMax;   // FP32 data too: entries far below their column maximum need the bits
-    const int64_t np = oz_rup(nj, kOzBM);
-    const int64_t rows_max = m < kOzRowChunk ? m : kOzRowChunk;
-    const int64_t mp_max = oz_rup(rows_max, kOzBK);
-    int8_t* sl = static_cast<int8_t*>(scratch);
-    unsigned long long* colmax = reinterpret_cast<unsigned long long*>(
-        static_cast<char*>(scratch) + oz_rup((int64_t)S * np * mp_max, 256));
+template <typename T>
+static void oz_operand(const void* src, int64_t sl, int64_t sr, int64_t L, int64_t R, unsigned long long* mx,
+                       cudaStream_t s) {
+    const int64_t r_per = 2048;
+    dim3 g((unsigned)((L + 255) / 256), (unsigned)((R + r_per - 1) / r_per));
+    k_oz_absmax<T><<<g, 256, 0, s>>>(static_cast<const T*>(src), sl, sr, L, R, r_per, mx);
+}
+template <typename T>
+static void oz_digits(const void* src, int64_t sl, int64_t sr, int64_t L, int64_t r_begin, int64_t rows,
+                      const unsigned long long* mx, int8_t* out, int64_t Lp, int64_t Kp, cudaStream_t s) {
+    dim3 g((unsigned)((Lp + 127) / 128), (unsigned)(Kp / 32));
+    k_oz_split<T><<<g, 128, 0, s>>>(static_cast<const T*>(src), sl, sr, L, r_begin, rows, mx, out, Lp, Kp);
+}
+
+int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0) return BICADMM_OK;
+    if (g.lower && g.M != g.N) return BICADMM_ERR_INVALID;
+    if (scratch_bytes < gemm_tc_scratch_bytes(g.M, g.N, g.K, g.same)) return BICADMM_ERR_INVALID;
+    const int64_t Mp = oz_rup(g.M, kOzBM), Np = g.same ? Mp : oz_rup(g.N, kOzBM);
+    const int64_t Kmax = g.K < kOzRowChunk ? g.K : kOzRowChunk;
+    const int64_t Kp_max = oz_rup(Kmax > 0 ? Kmax : 1, kOzBK);
+    char* base = static_cast<char*>(scratch);
+    int8_t* da = reinterpret_cast<int8_t*>(base);
+    size_t off = (size_t)oz_rup((int64_t)kOzSMax * Mp * Kp_max, 256);
+    int8_t* db = da;
+    if (!g.same) {
+        db = reinterpret_cast<int8_t*>(base + off);
+        off += (size_t)oz_rup((int64_t)kOzSMax * Np * Kp_max, 256);
+    }
+    unsigned long long* amax = reinterpret_cast<unsigned long long*>(base + off);
+    unsigned long long* bmax = g.same ? amax : amax + Mp;
     static bool attr = false;
     const size_t smem = kOzStages * kOzStageBytes + 1024;   // + alignment slack
     if (!attr) {
-        BIC_CUDA(cudaFuncSetAttribute(k_oz_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        BIC_CUDA(cudaFuncSetAttribute(k_oz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    // column scales over all rows
-    BIC_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * np, s));
-    {
-        const int64_t rows_per = 2048;
-        dim3 g((unsigned)((nj + 255) / 256), (unsigned)((m + rows_per - 1) / rows_per));
-        if (dtype == BICADMM_F64) k_oz_colmax<double><<<g, 256, 0, s>>>(static_cast<const double*>(A), lda, m, nj, rows_per, colmax);
-        else k_oz_colmax<float><<<g, 256, 0, s>>>(static_cast<const float*>(A), lda, m, nj, rows_per, colmax);
+    // per-row scales of both operands over the whole summed range
+    BIC_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long) * (size_t)(Mp + (g.same ? 0 : Np)), s));
+    if (g.K > 0) {
+        if (g.dtype == BICADMM_F64) oz_operand<double>(g.A, g.a_sl, g.a_sr, g.M, g.K, amax, s);
+        else oz_operand<float>(g.A, g.a_sl, g.a_sr, g.M, g.K, amax, s);
         BIC_LAUNCHED();
+        if (!g.same) {
+            if (g.dtype == BICADMM_F64) oz_operand<double>(g.B, g.b_sl, g.b_sr, g.N, g.K, bmax, s);
+            else oz_operand<float>(g.B, g.b_sl, g.b_sr, g.N, g.K, bmax, s);
+            BIC_LAUNCHED();
+        }
     }
-    const int64_t ntb = np / kOzBM;
-    const int64_t tiles = ntb * (ntb + 1);   // sum over bi of (2 bi + 2)
-    for (int64_t r_begin = 0; r_begin < m; r_begin += kOzRowChunk) {
-        const int64_t rows = m - r_begin < kOzRowChunk ? m - r_begin : kOzRowChunk;
-        const int64_t mp = oz_rup(rows, kOzBK);
-        dim3 gs((unsigned)((np + 127) / 128), (unsigned)(mp / 32));
-        if (dtype == BICADMM_F64)
-            k_oz_split<double><<<gs, 128, 0, s>>>(static_cast<const double*>(A), lda, m, nj, r_begin, rows, colmax, S, sl, np, mp);
-        else
-            k_oz_split<float><<<gs, 128, 0, s>>>(static_cast<const float*>(A), lda, m, nj, r_begin, rows, colmax, S, sl, np, mp);
-        BIC_LAUNCHED();
+    const int64_t ntb = Mp / kOzBM, ntj = oz_rup(g.N, kOzBN) / kOzBN;
+    const int64_t tiles = g.lower ? ntb * (ntb + 1) : ntb * ntj;   // lower: sum over bi of (2 bi + 2)
+    for (int64_t r_begin = 0; r_begin < (g.K > 0 ? g.K : 1); r_begin += kOzRowChunk) {
+        const int64_t rows = g.K - r_begin < kOzRowChunk ? g.K - r_begin : kOzRowChunk;
+        const int64_t Kp = oz_rup(rows > 0 ? rows : 1, kOzBK);
+        if (rows > 0) {
+            if (g.dtype == BICADMM_F64) oz_digits<double>(g.A, g.a_sl, g.a_sr, g.M, r_begin, rows, amax, da, Mp, Kp, s);
+            else oz_digits<float>(g.A, g.a_sl, g.a_sr, g.M, r_begin, rows, amax, da, Mp, Kp, s);
+            BIC_LAUNCHED();
+            if (!g.same) {
+                if (g.dtype == BICADMM_F64) oz_digits<double>(g.B, g.b_sl, g.b_sr, g.N, r_begin, rows, bmax, db, Np, Kp, s);
+                else oz_digits<float>(g.B, g.b_sl, g.b_sr, g.N, r_begin, rows, bmax, db, Np, Kp, s);
+                BIC_LAUNCHED();
+            }
+        }
         CUtensorMap tmA, tmB;
-        int rc = oz_map(&tmA, sl, S, np, mp, kOzBM);
-        if (!rc) rc = oz_map(&tmB, sl, S, np, mp, kOzBN);
+        int rc = oz_map(&tmA, da, Mp, Kp, kOzBM);
+        if (!rc) rc = oz_map(&tmB, db, Np, Kp, kOzBN);
         if (rc) return rc;
         OzArgs oa{};
-        oa.np = np; oa.mp = mp; oa.n = nj; oa.colmax = colmax; oa.S = S;
-        oa.alpha = alpha; oa.diag = diag; oa.G = G; oa.ldg = ldg; oa.accumulate = r_begin > 0;
-        k_oz_gram<<<(unsigned)tiles, kOzThreads, smem, s>>>(tmA, tmB, oa);
+        oa.M = g.M; oa.N = g.N; oa.Mp = Mp; oa.Np = Np; oa.Kp = rows > 0 ? Kp : 0; oa.ntj = ntj;
+        oa.lower = g.lower; oa.mirror = g.mirror; oa.k_lo = g.k_lo; oa.k_hi = g.k_hi;
+        oa.K = g.K; oa.r_begin = r_begin; oa.amax = amax; oa.bmax = bmax;
+        oa.alpha = g.alpha; oa.beta = r_begin > 0 ? 1.0 : g.beta; oa.diag = r_begin > 0 ? 0.0 : g.diag;
+        oa.C = g.C; oa.ldc = g.ldc;
+        k_oz_mm<<<(unsigned)tiles, kOzThreads, smem, s>>>(tmA, tmB, oa);
         BIC_LAUNCHED();
     }
     return BICADMM_OK;
+}
+
+int launch_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag, double* G,
+                   int64_t ldg, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+    if (m <= 0 || nj <= 0) return BICADMM_OK;
+    OzGemm g{};
+    g.M = nj; g.N = nj; g.K = m;
+    g.A = A; g.a_sl = 1; g.a_sr = lda;     // operand row l = column l of A, summed over rows
+    g.B = A; g.b_sl = 1; g.b_sr = lda;
+    g.same = true; g.dtype = dtype;
+    g.alpha = alpha; g.beta = 0.0; g.diag = diag; g.C = G; g.ldc = ldg;
+    g.lower = 1;
+    return launch_gemm_tc(g, scratch, scratch_bytes, s);
 }
 
 }  // namespace bic

@@ -88,6 +88,23 @@ int launch_loss(int loss, int dtype, int C, ProxNode* nodes, int nn, cudaStream_
 // FP64-accurate Gram on tcgen05 kind::i8 (Ozaki slices, k_gram_tc.cu): lower triangle of
 // alpha A^T A + diag I into G (FP64, ldg); scratch of gram_tc_scratch_bytes() (slices + scales)
 size_t gram_tc_scratch_bytes(int dtype, int64_t m, int64_t nj);
+// General FP64-accurate product on the same engine: C = alpha A_op B_op + beta C (+ diag I),
+// A_op(i, k) = A[i a_sl + k a_sr] (M x K), B_op(k, j) = B[j b_sl + k b_sr] (K x N), FP64 C.
+// k_lo / k_hi: structural zeros skipped per tile (exact): k_lo 1: A_op(i, k) = 0 for k < i,
+// 2: B_op(k, j) = 0 for k < j, 3: both (k >= max(i, j)); k_hi 1: A_op(i, k) = 0 for k > i,
+// 2: B_op(k, j) = 0 for k > j.  lower: M == N, entries j <= i only (mirror: and C[j][i]).
+struct OzGemm {
+    int64_t M, N, K;
+    const void* A; int64_t a_sl, a_sr;
+    const void* B; int64_t b_sl, b_sr;
+    bool same;        // B_op = A_op^T (one digit set)
+    int dtype;        // of A and B
+    double alpha, beta, diag;
+    double* C; int64_t ldc;
+    int lower, mirror, k_lo, k_hi;
+};
+size_t gemm_tc_scratch_bytes(int64_t M, int64_t N, int64_t K, bool same);
+int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStream_t s);
 bool gram_tc_enabled();
 int launch_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha, double diag, double* G,
                    int64_t ldg, void* scratch, size_t scratch_bytes, cudaStream_t s);

@@ -92,6 +92,26 @@ extern "C" size_t bicadmm_op_gram_tc_ws(int dtype, int64_t m, int64_t nj) {
     return (m < 1 || nj < 1) ? 0 : gram_tc_scratch_bytes(dtype, m, nj);
 }
 
+extern "C" size_t bicadmm_op_gemm_tc_ws(int64_t M, int64_t N, int64_t K, int same) {
+    return (M < 1 || N < 1 || K < 0) ? 0 : gemm_tc_scratch_bytes(M, N, K, same != 0);
+}
+
+extern "C" int bicadmm_op_gemm_tc(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t a_sl,
+                                  int64_t a_sr, const void* B, int64_t b_sl, int64_t b_sr, int same, double alpha,
+                                  double beta, double diag, double* C, int64_t ldc, int flags, void* ws,
+                                  size_t ws_bytes, void* stream) {
+    if (M < 1 || N < 1 || K < 0 || !A || (!same && !B) || !C || ldc < N || !ws) return BICADMM_ERR_INVALID;
+    if (dtype != BICADMM_F64 && dtype != BICADMM_F32) return BICADMM_ERR_INVALID;
+    OzGemm g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.a_sl = a_sl; g.a_sr = a_sr;
+    g.same = same != 0;
+    g.B = g.same ? A : B; g.b_sl = g.same ? a_sl : b_sl; g.b_sr = g.same ? a_sr : b_sr;
+    g.dtype = dtype; g.alpha = alpha; g.beta = beta; g.diag = diag; g.C = C; g.ldc = ldc;
+    g.lower = flags & 1; g.mirror = (flags >> 1) & 1; g.k_lo = (flags >> 4) & 3; g.k_hi = (flags >> 8) & 3;
+    return launch_gemm_tc(g, ws, ws_bytes, (cudaStream_t)stream);
+}
+
 extern "C" int bicadmm_op_gram_tc(int dtype, int64_t m, int64_t nj, const void* A, int64_t lda, double alpha,
                                   double diag, double* G, int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
     if (m < 1 || nj < 1 || lda < nj || !A || !G || ldg < nj || !ws) return BICADMM_ERR_INVALID;

@@ -170,6 +170,79 @@ def test_gram_tc(bc, m, nj, dt):
     assert np.all(Gn[np.triu_indices(nj, 1)] == 7.0)     # upper triangle untouched
 
 
+GEMM_TC_CASES = [
+    # name, M, N, K, layout, flags, beta
+    ("rect_rowmajor", 300, 200, 500, "nn", 0, 0.0),
+    ("rect_beta_ragged", 131, 77, 33, "nt", 0, -0.5),
+    ("syrk_lower", 260, 260, 190, "nt", 1, 1.0),
+    ("tri_hi_B", 200, 250, 250, "trB_hi", 2 << 8, 0.0),      # X = F21 W11^T (B_op(k,j)=0 for k > j)
+    ("tri_lo_B", 200, 250, 250, "trB_lo", 2 << 4, 0.0),      # X = L21 W11 (B_op(k,j)=0 for k < j)
+    ("tri_hi_A", 260, 140, 260, "trA_hi", 1 << 8, 0.0),      # W21 = -W22 X (A_op(i,k)=0 for k > i)
+    ("tri_gram_mirror", 333, 333, 333, "wtw", 1 | 2 | (3 << 4), 0.0),   # H = W^T W
+    ("long_k_chunks", 64, 96, 70000, "nn", 0, 0.0),
+]
+
+
+@pytest.mark.parametrize("case", GEMM_TC_CASES, ids=[c[0] for c in GEMM_TC_CASES])
+def test_gemm_tc(bc, case):
+    # the a0 factor's large products on the tcgen05 Ozaki engine vs the FP64 definition, with
+    # the zero structures whose tiles it skips; error relative to ||A_op(i,:)|| ||B_op(:,j)||
+    name, M, N, K, layout, flags, beta = case
+    rng = np.random.default_rng(M + N + K)
+    lo_scale = np.exp(rng.uniform(-4, 4, size=max(M, N, K)))
+    A = rng.normal(size=(M, K)) * lo_scale[:M, None]
+    B = rng.normal(size=(K, N)) * lo_scale[None, :N]
+    same = 0
+    if layout == "trB_hi":
+        B = np.tril(rng.normal(size=(N, K))).T          # B_op(k,j) = W[j][k], W lower
+    elif layout == "trB_lo":
+        B = np.tril(rng.normal(size=(K, N)))            # B_op(k,j) = W[k][j], W lower
+    elif layout == "trA_hi":
+        A = np.tril(rng.normal(size=(M, K)))            # A_op(i,k) = W[i][k], W lower
+    elif layout == "wtw":
+        W = np.tril(rng.normal(size=(K, M)) * lo_scale[None, :M])
+        A, B, same = W.T, W, 1
+    C0 = rng.normal(size=(M, N))
+    ref = A @ B + beta * C0
+    # device operands in the layouts the factor uses
+    if layout == "nt":                                  # B_op(k,j) = Bs[j][k] (row-major N x K)
+        Bs = torch.tensor(np.ascontiguousarray(B.T), device="cuda")
+        b_sl, b_sr = Bs.stride(0), 1
+    elif layout == "trB_hi":
+        Bs = torch.tensor(np.ascontiguousarray(B.T), device="cuda")
+        b_sl, b_sr = Bs.stride(0), 1
+    else:                                               # row-major K x N
+        Bs = torch.tensor(np.ascontiguousarray(B), device="cuda")
+        b_sl, b_sr = 1, Bs.stride(0)
+    if layout == "wtw":                                 # A_op(i,k) = W[k][i]
+        As = torch.tensor(np.ascontiguousarray(W), device="cuda")
+        a_sl, a_sr = 1, As.stride(0)
+    else:
+        As = torch.tensor(np.ascontiguousarray(A), device="cuda")
+        a_sl, a_sr = As.stride(0), 1
+    C = torch.tensor(C0, device="cuda")
+    if flags & 1:
+        C.copy_(torch.tensor(np.where(np.tril(np.ones((M, N))) > 0, C0, 7.0), device="cuda"))
+    L = bc.lib()
+    wsb = L.bicadmm_op_gemm_tc_ws(M, N, K, same)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    bc.check(L.bicadmm_op_gemm_tc(bc.F64, M, N, K, _p(As), a_sl, a_sr, _p(Bs), b_sl, b_sr, same, 1.0, beta, 0.0,
+                                  _p(C), C.stride(0), flags, _p(ws), wsb, _s()))
+    torch.cuda.synchronize()
+    Cn = C.cpu().numpy()
+    scale = np.outer(np.linalg.norm(A, axis=1), np.linalg.norm(B, axis=0)) + abs(beta) * np.abs(C0)
+    err = np.abs(Cn - ref) / np.maximum(scale, 1e-300)
+    if flags & 1:
+        lo = np.tril_indices(M)
+        assert np.max(err[lo]) <= 3e-14
+        if flags & 2:
+            assert np.array_equal(Cn, Cn.T)
+        else:
+            assert np.all(Cn[np.triu_indices(M, 1)] == 7.0)
+    else:
+        assert np.max(err) <= 3e-14
+
+
 ZT_CASES = []
 _rng = np.random.default_rng(42)
 for _k in range(12):
