@@ -557,10 +557,13 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
         h->gram = b.arr<double>(h->gram_stride * h->fbatch);
         h->fws = b.arr<double>(h->fws_stride * h->fbatch);
         // tcgen05 Ozaki-scheme Gram (k_gram_tc.cu) for tall blocks: slices of up to 32,768 rows
+        // and the factor's large products (factor_inverse_batched), sharing the scratch
         size_t gtc = 0;
         if (gram_tc_enabled())
-            for (auto& L : h->blk)
+            for (auto& L : h->blk) {
                 if (!L.fat) gtc = std::max(gtc, gram_tc_scratch_bytes(P->dtype, L.m, L.nj));
+                gtc = std::max(gtc, factor_tc_scratch_bytes(L.kd));
+            }
         h->gtc_bytes = gtc;
         h->gtc_ws = gtc ? b.take(gtc) : nullptr;
     }
@@ -952,7 +955,7 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             jobs.push_back(FactorJob{L.kd, G, ldg, L.hpack ? (void*)G : L.H, L.hpack ? ldg : L.ldh,
                                      L.hpack ? (int)BICADMM_F64 : P->dtype, h->fws + k * h->fws_stride});
         }
-        if (!rc) rc = factor_inverse_batched(jobs.data(), (int)jobs.size(), h->st);
+        if (!rc) rc = factor_inverse_batched(jobs.data(), (int)jobs.size(), h->st, h->gtc_ws, h->gtc_bytes);
         for (int k = 0; k < nb && !rc; ++k) {
             LBlock& L = h->blk[b0 + k];
             if (L.hpack) rc = launch_symv_pack(P->dtype, L.kd, h->gram + k * h->gram_stride, rup(L.kd, 8), L.H, h->st);

@@ -299,7 +299,43 @@ struct RecJob {
     int* info;
 };
 
-static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStream_t s) {
+// Large products of the recursion go to the tcgen05 Ozaki engine (k_gram_tc.cu: FP64-accurate,
+// ~2x the DMMA rate at these sizes), one job at a time through the shared scratch; the small
+// ones stay on the batched DMMA kernel.  Structural zeros (k_lo / k_hi / tri_k) are skipped
+// exactly on both paths.
+struct FactorTc {
+    void* ws = nullptr;
+    size_t bytes = 0;
+};
+constexpr double kTcMinVolume = 8.0e9;   // M N K (~2000^3): below it the DMMA batch wins
+
+template <bool AK, bool BK_>
+static int gemm_factor(const GemmArgs* ga, int nj, const FactorTc* tc, cudaStream_t s) {
+    const GemmArgs& g0 = ga[0];
+    if (tc && tc->ws && (double)g0.M * (double)g0.N * (double)g0.K >= kTcMinVolume &&
+        gemm_tc_scratch_bytes(g0.M, g0.N, g0.K, false) <= tc->bytes) {
+        for (int k = 0; k < nj; ++k) {
+            const GemmArgs& g = ga[k];
+            OzGemm o{};
+            o.M = g.M; o.N = g.N; o.K = g.K;
+            o.A = g.A;
+            o.a_sl = AK ? g.lda : 1; o.a_sr = AK ? 1 : g.lda;      // A(i,k): AK -> A[i lda + k]
+            o.B = g.B;
+            o.b_sl = BK_ ? g.ldb : 1; o.b_sr = BK_ ? 1 : g.ldb;    // B(k,j): BK -> B[j ldb + k]
+            o.same = o.A == o.B && o.a_sl == o.b_sl && o.a_sr == o.b_sr;
+            o.dtype = BICADMM_F64;
+            o.alpha = g.alpha; o.beta = g.beta; o.diag = g.diag; o.C = static_cast<double*>(g.C); o.ldc = g.ldc;
+            o.lower = g.lower_only; o.mirror = g.mirror;
+            o.k_lo = g.tri_k ? 3 : g.k_lo; o.k_hi = g.k_hi;
+            const int rc = launch_gemm_tc(o, tc->ws, tc->bytes, s);
+            if (rc) return rc;
+        }
+        return BICADMM_OK;
+    }
+    return gemm_batched<double, double, AK, BK_>(ga, nj, s);
+}
+
+static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, const FactorTc* tc, cudaStream_t s) {
     if (n <= NB) {
         DiagBatch db{};
         for (int k = 0; k < nj; ++k) {
@@ -314,7 +350,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
     int64_t n1 = (n / 2 + NB - 1) / NB * NB;
     if (n1 >= n) n1 = n - NB;
     const int64_t n2 = n - n1;
-    int rc = chol_inv_rec(J, nj, n1, off, s);
+    int rc = chol_inv_rec(J, nj, n1, off, tc, s);
     if (rc) return rc;
     GemmArgs ga[kMaxBatch];
     // X = F21 W11^T  (n2 x n1 x n1): A(i,k) = F21[i][k] (K-fast), B(k,j) = W11[j][k] (K-fast)
@@ -326,7 +362,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.C = J[k].X; g.ldc = J[k].ldw; g.k_hi = 2;
         ga[k] = g;
     }
-    rc = gemm_batched<double, double, true, true>(ga, nj, s);
+    rc = gemm_factor<true, true>(ga, nj, tc, s);
     if (rc) return rc;
     for (int k = 0; k < nj; ++k)   // L21 = X
         BIC_CUDA(cudaMemcpy2DAsync(J[k].F + (off + n1) * J[k].ldf + off, sizeof(double) * J[k].ldf, J[k].X,
@@ -340,9 +376,9 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.C = J[k].F + (off + n1) * J[k].ldf + off + n1; g.ldc = J[k].ldf; g.lower_only = 1;
         ga[k] = g;
     }
-    rc = gemm_batched<double, double, true, true>(ga, nj, s);
+    rc = gemm_factor<true, true>(ga, nj, tc, s);
     if (rc) return rc;
-    rc = chol_inv_rec(J, nj, n2, off + n1, s);
+    rc = chol_inv_rec(J, nj, n2, off + n1, tc, s);
     if (rc) return rc;
     // X = L21 W11 (n2 x n1 x n1): A(i,k) = L21[i][k], B(k,j) = W11[k][j] (N-fast)
     for (int k = 0; k < nj; ++k) {
@@ -353,7 +389,7 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.C = J[k].X; g.ldc = J[k].ldw; g.k_lo = 2;
         ga[k] = g;
     }
-    rc = gemm_batched<double, double, true, false>(ga, nj, s);
+    rc = gemm_factor<true, false>(ga, nj, tc, s);
     if (rc) return rc;
     // W21 = -W22 X (n2 x n1 x n2): A(i,k) = W22[i][k], B(k,j) = X[k][j]
     for (int k = 0; k < nj; ++k) {
@@ -364,15 +400,17 @@ static int chol_inv_rec(const RecJob* J, int nj, int64_t n, int64_t off, cudaStr
         g.C = J[k].W + (off + n1) * J[k].ldw + off; g.ldc = J[k].ldw; g.k_hi = 1;
         ga[k] = g;
     }
-    return gemm_batched<double, double, true, false>(ga, nj, s);
+    return gemm_factor<true, false>(ga, nj, tc, s);
 }
+
+size_t factor_tc_scratch_bytes(int64_t n) { return gemm_tc_scratch_bytes(n, n, n, false); }
 
 static bool factor_rec_enabled() {
     static const bool on = [] { const char* e = getenv("BICADMM_FACTOR_REC"); return !(e && atoi(e) == 0); }();
     return on;
 }
 
-static int factor_inverse_rec(const FactorJob* jobs, int njobs, cudaStream_t s) {
+static int factor_inverse_rec(const FactorJob* jobs, int njobs, const FactorTc* tc, cudaStream_t s) {
     const int64_t n = jobs[0].n;
     const int hdtype = jobs[0].hdtype;
     RecJob J[kMaxBatch];
@@ -392,7 +430,7 @@ static int factor_inverse_rec(const FactorJob* jobs, int njobs, cudaStream_t s) 
                                       (int)(sizeof(double) * 2 * NB * (NB + 1))));
         attr_set = true;
     }
-    int rc = chol_inv_rec(J, njobs, n, 0, s);
+    int rc = chol_inv_rec(J, njobs, n, 0, tc, s);
     if (rc) return rc;
     GemmArgs ga[kMaxBatch];
     for (int k = 0; k < njobs; ++k) {   // H = W^T W (W lower: K range from max(m0, n0)); lower tiles mirrored
@@ -402,7 +440,7 @@ static int factor_inverse_rec(const FactorJob* jobs, int njobs, cudaStream_t s) 
         g.lower_only = 1; g.mirror = 1; g.tri_k = 1;
         ga[k] = g;
     }
-    rc = hdtype == BICADMM_F64 ? gemm_batched<double, double, false, false>(ga, njobs, s)
+    rc = hdtype == BICADMM_F64 ? gemm_factor<false, false>(ga, njobs, tc, s)
                                : gemm_batched<double, float, false, false>(ga, njobs, s);
     if (rc) return rc;
     int hinfo[kMaxBatch] = {};
@@ -413,14 +451,17 @@ static int factor_inverse_rec(const FactorJob* jobs, int njobs, cudaStream_t s) 
     return BICADMM_OK;
 }
 
-int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s) {
+int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s, void* tc_ws, size_t tc_bytes) {
+    FactorTc tc;
+    tc.ws = gram_tc_enabled() ? tc_ws : nullptr;
+    tc.bytes = tc_bytes;
     if (njobs > 0 && factor_rec_enabled()) {
         // recursive (large-GEMM) variant, one lockstep batch per distinct size
         std::vector<FactorJob> rest(jobs, jobs + njobs);
         while (!rest.empty()) {
             std::vector<FactorJob> same, other;
             for (auto& j : rest) (j.n == rest[0].n && j.hdtype == rest[0].hdtype && same.size() < kMaxBatch ? same : other).push_back(j);
-            const int rc = factor_inverse_rec(same.data(), (int)same.size(), s);
+            const int rc = factor_inverse_rec(same.data(), (int)same.size(), &tc, s);
             if (rc) return rc;
             rest.swap(other);
         }

@@ -65,6 +65,20 @@ __global__ void k_oz_absmax(const T* __restrict__ src, int64_t sl, int64_t sr, i
     atomicMax(mx + l, (unsigned long long)__double_as_longlong(m));
 }
 
+// Operand rows contiguous (sr == 1): one warp per row, coalesced, shuffle max
+template <typename T>
+__global__ void k_oz_absmax_rows(const T* __restrict__ src, int64_t sl, int64_t L, int64_t R,
+                                 unsigned long long* __restrict__ mx) {
+    const int64_t l = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (l >= L) return;
+    const int lane = threadIdx.x & 31;
+    double m = 0.0;
+    for (int64_t r = lane; r < R; r += 32) m = fmax(m, fabs((double)src[l * sl + r]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) mx[l] = (unsigned long long)__double_as_longlong(m);
+}
+
 // ----------------------------------------------------------------------------- split
 // Thread = (operand row l, 32 summed indices): digits written as out[s][l][r] (K-major,
 // row stride Kp), 32 bytes per digit per thread.  r >= rows and l >= L are zero.
@@ -91,6 +105,50 @@ __global__ void k_oz_split(const T* __restrict__ src, int64_t sl, int64_t sr, in
             const double t = a * 128.0;               // exact
             const double d = rint(t);                 // |d| <= 127 (s = 1), <= 64 (s > 1)
             a = t - d;                                // exact, |a| <= 1/2
+            const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
+            pk[s][k >> 2] |= byte << (8 * (k & 3));
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < kOzSMax; ++s) {
+        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * Lp + l) * Kp + rg);
+        dst[0] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
+        dst[1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
+    }
+}
+
+// sr == 1 (operand rows contiguous): the CTA's 128 rows x 32 summed indices are staged
+// through shared memory by coalesced row reads (row stride 33 doubles: conflict-free), then
+// digitised as above.
+template <typename T>
+__global__ void __launch_bounds__(128) k_oz_split_rows(const T* __restrict__ src, int64_t sl, int64_t L, int64_t r_begin,
+                                                       int64_t rows, const unsigned long long* __restrict__ mx,
+                                                       int8_t* __restrict__ out, int64_t Lp, int64_t Kp) {
+    __shared__ double tile[128][33];
+    const int64_t l0 = (int64_t)blockIdx.x * 128;
+    const int64_t rg = (int64_t)blockIdx.y * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int q = warp; q < 128; q += 4) {
+        const int64_t l = l0 + q, r = rg + lane;
+        tile[q][lane] = (l < L && r < rows) ? (double)src[l * sl + r_begin + r] : 0.0;
+    }
+    __syncthreads();
+    const int64_t l = l0 + threadIdx.x;
+    if (l >= Lp || rg >= Kp) return;
+    const int e = l < L ? oz_exp(__longlong_as_double((long long)mx[l])) : 0;
+    uint32_t pk[kOzSMax][8];
+#pragma unroll
+    for (int s = 0; s < kOzSMax; ++s)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pk[s][q] = 0u;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        double a = scalbn(tile[threadIdx.x][k], -e);
+#pragma unroll
+        for (int s = 0; s < kOzSMax; ++s) {
+            const double t = a * 128.0;
+            const double d = rint(t);
+            a = t - d;
             const uint32_t byte = (uint32_t)(uint8_t)(int8_t)(int)d;
             pk[s][k >> 2] |= byte << (8 * (k & 3));
         }
@@ -389,7 +447,11 @@ bool gram_tc_enabled() {
 template <typename T>
 static void oz_operand(const void* src, int64_t sl, int64_t sr, int64_t L, int64_t R, unsigned long long* mx,
                        cudaStream_t s) {
-    const int64_t r_per = 2048;
+    if (sr == 1 && sl != 1) {
+        k_oz_absmax_rows<T><<<(unsigned)((L + 7) / 8), 256, 0, s>>>(static_cast<const T*>(src), sl, L, R, mx);
+        return;
+    }
+    const int64_t r_per = L >= 16384 ? 2048 : 256;   // enough CTAs for narrow operands
     dim3 g((unsigned)((L + 255) / 256), (unsigned)((R + r_per - 1) / r_per));
     k_oz_absmax<T><<<g, 256, 0, s>>>(static_cast<const T*>(src), sl, sr, L, R, r_per, mx);
 }
@@ -397,7 +459,10 @@ template <typename T>
 static void oz_digits(const void* src, int64_t sl, int64_t sr, int64_t L, int64_t r_begin, int64_t rows,
                       const unsigned long long* mx, int8_t* out, int64_t Lp, int64_t Kp, cudaStream_t s) {
     dim3 g((unsigned)((Lp + 127) / 128), (unsigned)(Kp / 32));
-    k_oz_split<T><<<g, 128, 0, s>>>(static_cast<const T*>(src), sl, sr, L, r_begin, rows, mx, out, Lp, Kp);
+    if (sr == 1 && sl != 1)
+        k_oz_split_rows<T><<<g, 128, 0, s>>>(static_cast<const T*>(src), sl, L, r_begin, rows, mx, out, Lp, Kp);
+    else
+        k_oz_split<T><<<g, 128, 0, s>>>(static_cast<const T*>(src), sl, sr, L, r_begin, rows, mx, out, Lp, Kp);
 }
 
 int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStream_t s) {

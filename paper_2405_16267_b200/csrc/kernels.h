@@ -129,7 +129,11 @@ struct FactorJob {
     double* ws;
 };
 // All jobs' blocked Cholesky / inverse steps run in lockstep, up to 8 GEMMs per launch.
-int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s);
+// tc_ws (optional): scratch for the large products on the tcgen05 Ozaki engine
+// (>= factor_tc_scratch_bytes(n) for the largest n); null -> DMMA only.
+int factor_inverse_batched(const FactorJob* jobs, int njobs, cudaStream_t s, void* tc_ws = nullptr,
+                           size_t tc_bytes = 0);
+size_t factor_tc_scratch_bytes(int64_t n);
 int factor_inverse(int64_t nj, double* G, int64_t ldg, void* H, int64_t ldh, int dtype,
                    double* ws, cudaStream_t s);
 
