@@ -22,14 +22,14 @@
 // tcgen05.cp + slot-reuse waits cost more than that saves.)
 //
 // Pipeline per CTA (one 128 x 64 tile of G, lower triangle of tiles):
-//   warp 5    : one thread issues the TMA copies (cp.async.bulk.tensor.2d, SWIZZLE_32B) of
+//   warp 5    : one thread issues the bulk copies (cp.async.bulk, one contiguous 4 KB / 2 KB
+//               block per digit tile: the digits are stored pre-swizzled, SWIZZLE_32B) of
 //               the S slices of 32 rows x (128 + 64) columns into a 5-stage ring
 //   warp 4    : one thread issues S(S+1)/2 tcgen05.mma (M 128, N 64, K 32) per stage,
 //               commits to the stage's "empty" barrier and, per 16,384-row round, to
 //               "acc_full"
 //   warps 0-3 : the TMEM epilogue (tcgen05.ld of the 7 accumulators per round)
 // The slices are produced once per block by k_oz_split (column-major int8, zero padded).
-#include <cuda.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -80,8 +80,11 @@ __global__ void k_oz_absmax_rows(const T* __restrict__ src, int64_t sl, int64_t 
 }
 
 // ----------------------------------------------------------------------------- split
-// Thread = (operand row l, 32 summed indices): digits written as out[s][l][r] (K-major,
-// row stride Kp), 32 bytes per digit per thread.  r >= rows and l >= L are zero.
+// Thread = (operand row l, 32 summed indices): digits written K-chunk major,
+// out[s][r / 32][l][r % 32] (32 bytes per digit per thread; adjacent rows l adjacent, so the
+// stores coalesce and a tile of rows is one contiguous block); the two 16-byte halves of a
+// row piece are stored in the SWIZZLE_32B order of the UMMA descriptor (chunk ^= bit 2 of
+// the row), so a plain bulk copy lands in the layout the MMA reads.  r >= rows, l >= L: 0.
 template <typename T>
 __global__ void k_oz_split(const T* __restrict__ src, int64_t sl, int64_t sr, int64_t L, int64_t r_begin,
                            int64_t rows, const unsigned long long* __restrict__ mx, int8_t* __restrict__ out,
@@ -111,9 +114,10 @@ __global__ void k_oz_split(const T* __restrict__ src, int64_t sl, int64_t sr, in
     }
 #pragma unroll
     for (int s = 0; s < kOzSMax; ++s) {
-        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * Lp + l) * Kp + rg);
-        dst[0] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
-        dst[1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
+        uint4* dst = reinterpret_cast<uint4*>(out + (((int64_t)s * (Kp / 32) + rg / 32) * Lp + l) * 32);
+        const int sw = (int)((l >> 2) & 1);   // SWIZZLE_32B: 16-byte chunk ^= bit 2 of the row
+        dst[sw] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
+        dst[sw ^ 1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
     }
 }
 
@@ -155,14 +159,15 @@ __global__ void __launch_bounds__(128) k_oz_split_rows(const T* __restrict__ src
     }
 #pragma unroll
     for (int s = 0; s < kOzSMax; ++s) {
-        uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)s * Lp + l) * Kp + rg);
-        dst[0] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
-        dst[1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
+        uint4* dst = reinterpret_cast<uint4*>(out + (((int64_t)s * (Kp / 32) + rg / 32) * Lp + l) * 32);
+        const int sw = (int)((l >> 2) & 1);   // SWIZZLE_32B: 16-byte chunk ^= bit 2 of the row
+        dst[sw] = make_uint4(pk[s][0], pk[s][1], pk[s][2], pk[s][3]);
+        dst[sw ^ 1] = make_uint4(pk[s][4], pk[s][5], pk[s][6], pk[s][7]);
     }
 }
 
 // ----------------------------------------------------------------------------- GEMM
-// Operands by TMA (cp.async.bulk.tensor.2d, SWIZZLE_32B: one K = 32-byte row per column,
+// Operands by bulk copy (pre-swizzled SWIZZLE_32B: one K = 32-byte row per column,
 // 8-column atoms of 256 B), 4-stage ring, one tcgen05.mma (M 128, N 64, K 32) per slice
 // pair per stage.
 __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
@@ -193,6 +198,11 @@ __device__ __forceinline__ void oz_mbar_wait_sleep(uint64_t* b, uint32_t parity)
         if (it > (1ll << 26)) asm volatile("trap;");
     }
 }
+// plain bulk copy global -> shared (one contiguous block), completing on an mbarrier
+__device__ __forceinline__ void oz_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(oz_smem(dst)), "l"(src), "r"(bytes), "r"(oz_smem(bar)) : "memory");
+}
 __device__ __forceinline__ void oz_mbar_arrive(uint64_t* b) {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(oz_smem(b)) : "memory");
 }
@@ -221,6 +231,7 @@ struct OzArgs {
     int k_lo, k_hi;          // zero structure of the operands (launch_gemm_tc), absolute indices
     int64_t K, r_begin;      // total summed length; this chunk starts at r_begin
     const unsigned long long *amax, *bmax;   // per-row maxima of the A / B operands
+    const int8_t *da, *db;   // digits, [S][Kp / 32][Lp][32 bytes], 32-byte rows pre-swizzled
     double alpha, beta, diag;
     double* C;
     int64_t ldc;
@@ -228,8 +239,7 @@ struct OzArgs {
 
 // One 128 x 64 tile of C = alpha A B^T-ish (both operands K-major digit slices) + beta C + diag I
 __global__ void __launch_bounds__(kOzThreads, 1)
-    k_oz_mm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            const __grid_constant__ OzArgs a) {
+    k_oz_mm(const __grid_constant__ OzArgs a) {
     extern __shared__ __align__(1024) uint8_t oz_sm_raw[];
     uint8_t* oz_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_sm_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[kOzStages], empty[kOzStages], acc_full, acc_empty;
@@ -288,18 +298,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_smem(&full[sb])),
                              "r"(bytes_stage) : "memory");
                 uint8_t* base = oz_sm + (size_t)sb * kOzStageBytes;
-                const int k0 = (st0 + q) * kOzBK;
+                const int64_t kc = st0 + q, KC = a.Kp / kOzBK;
 #pragma unroll
                 for (int s = 0; s < kOzSMax; ++s) {
-                    const int ra = (int)(s * a.Mp + i0), rbb = (int)(s * a.Np + j0);
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                        ::"r"(oz_smem(base + (size_t)s * kOzBM * kOzBK)), "l"(&tmA), "r"(k0), "r"(ra),
-                          "r"(oz_smem(&full[sb])) : "memory");
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                        ::"r"(oz_smem(base + (size_t)kOzSMax * kOzBM * kOzBK + (size_t)s * kOzBN * kOzBK)), "l"(&tmB),
-                          "r"(k0), "r"(rbb), "r"(oz_smem(&full[sb])) : "memory");
+                    const int64_t ra = (s * KC + kc) * a.Mp + i0, rbb = (s * KC + kc) * a.Np + j0;
+                    oz_bulk(base + (size_t)s * kOzBM * kOzBK, a.da + ra * kOzBK, kOzBM * kOzBK, &full[sb]);
+                    oz_bulk(base + (size_t)kOzSMax * kOzBM * kOzBK + (size_t)s * kOzBN * kOzBK, a.db + rbb * kOzBK,
+                            kOzBN * kOzBK, &full[sb]);
                 }
             }
         }
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         if (i < a.M) {
             const int ei = oz_exp(__longlong_as_double((long long)a.amax[i]));
             double* crow = a.C + i * a.ldc;
-#pragma unroll 4
+#pragma unroll
             for (int c = 0; c < kOzBN; ++c) {
                 const int64_t j = j0 + c;
                 if (j >= a.N || (a.lower && j > i)) continue;
@@ -391,6 +396,204 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ----------------------------------------------------------------------------- N = 128, two passes
+// At N = 64 a tcgen05.mma kind::i8 costs ~48 cycles instead of 32 (tools/tc_i8_rate.cu);
+// N = 128 runs at the full rate (64 cycles for twice the work).  Seven 128 x 128 int32
+// accumulators do not fit the 512 TMEM columns, so each tile streams its summed range
+// twice: pass 0 the weights 2..5 (digits 1..4, 10 products, 4 accumulators = 512
+// columns), pass 1 the weights 6..8 (all digits, 18 products, 3 accumulators).  The FP64
+// result is the same sum in another fixed order.  8 epilogue warps (lane quarter w & 3,
+// column half w >> 2), 1 MMA warp, 1 TMA warp.
+constexpr int kOz2BN = 128;
+constexpr int kOz2Stages = 4;
+constexpr int kOz2Threads = 320;
+constexpr size_t kOz2Slice = (size_t)kOz2BN * kOzBK;                     // 4 KB per digit tile
+constexpr size_t kOz2StageBytes = (size_t)kOzSMax * 2 * kOz2Slice;      // 56 KB
+
+__device__ __forceinline__ void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ constexpr int oz2_nslice(int pass) { return pass == 0 ? 4 : kOzSMax; }
+
+__global__ void __launch_bounds__(kOz2Threads, 1)
+    k_oz_mm128(const __grid_constant__ OzArgs a) {
+    extern __shared__ __align__(1024) uint8_t oz_sm_raw[];
+    uint8_t* oz_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_sm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kOz2Stages], empty[kOz2Stages], acc_full, acc_empty;
+    __shared__ uint32_t tmem_base;
+    int64_t bi, bj;
+    if (a.lower) {   // 128 x 128 tiles with bj <= bi
+        int64_t t = blockIdx.x;
+        bi = 0;
+        while (t >= bi + 1) { t -= bi + 1; ++bi; }
+        bj = t;
+    } else {
+        bi = (int64_t)blockIdx.x / a.ntj;
+        bj = (int64_t)blockIdx.x % a.ntj;
+    }
+    const int64_t i0 = bi * kOzBM, j0 = bj * kOz2BN;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int64_t klo = 0, khi = a.K;
+    if (a.k_lo == 1) klo = i0;
+    if (a.k_lo == 2) klo = j0;
+    if (a.k_lo == 3) klo = i0 > j0 ? i0 : j0;
+    if (a.k_hi == 1 && i0 + kOzBM < khi) khi = i0 + kOzBM;
+    if (a.k_hi == 2 && j0 + kOz2BN < khi) khi = j0 + kOz2BN;
+    klo = (klo > a.r_begin ? klo : a.r_begin) - a.r_begin;
+    khi = (khi < a.r_begin + a.Kp ? khi : a.r_begin + a.Kp) - a.r_begin;
+    const int st0 = (int)(klo / kOzBK);
+    const int st1 = khi > klo ? (int)((khi + kOzBK - 1) / kOzBK) : st0;
+    const int nstage = st1 - st0;
+    const int nround = (nstage + kOzRoundStages - 1) / kOzRoundStages;   // per pass
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_smem(&tmem_base)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kOz2Stages; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&empty[s])));
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&acc_full)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_smem(&acc_empty)), "r"(256));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 9) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int q = 0;   // stage counter over both passes
+            for (int pass = 0; pass < 2; ++pass) {
+                const int ns = oz2_nslice(pass);
+                for (int st = 0; st < nstage; ++st, ++q) {
+                    const int sb = q % kOz2Stages;
+                    if (q >= kOz2Stages) oz_mbar_wait(&empty[sb], (uint32_t)((q / kOz2Stages - 1) & 1));
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_smem(&full[sb])),
+                                 "r"((uint32_t)(ns * 2 * kOz2Slice)) : "memory");
+                    uint8_t* base = oz_sm + (size_t)sb * kOz2StageBytes;
+                    const int64_t kc = st0 + st, KC = a.Kp / kOzBK;
+                    for (int s = 0; s < ns; ++s) {
+                        const int64_t ra = (s * KC + kc) * a.Mp + i0, rbb = (s * KC + kc) * a.Np + j0;
+                        oz_bulk(base + (size_t)s * kOz2Slice, a.da + ra * kOzBK, (uint32_t)kOz2Slice, &full[sb]);
+                        oz_bulk(base + (size_t)(kOzSMax + s) * kOz2Slice, a.db + rbb * kOzBK, (uint32_t)kOz2Slice, &full[sb]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            // idesc: S32 accumulate, s8 x s8, K-major A and B, N = 128, M = 128
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOz2BN >> 3) << 17) |
+                                   ((uint32_t)(kOzBM >> 4) << 24);
+            const uint32_t smem0 = oz_smem(oz_sm);
+            int q = 0, rglob = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                const int wlo = pass == 0 ? 2 : 6, whi = pass == 0 ? 5 : kOzSMax + 1;
+                int st = 0;
+                for (int rd = 0; rd < nround; ++rd, ++rglob) {
+                    if (rglob > 0) oz_mbar_wait(&acc_empty, (uint32_t)((rglob - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const int st_end = (rd + 1) * kOzRoundStages < nstage ? (rd + 1) * kOzRoundStages : nstage;
+                    const int st_begin = st;
+                    for (; st < st_end; ++st, ++q) {
+                        const int sb = q % kOz2Stages;
+                        oz_mbar_wait(&full[sb], (uint32_t)((q / kOz2Stages) & 1));
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint64_t dS = oz_desc(smem0 + (uint32_t)(sb * kOz2StageBytes));
+                        const uint32_t first = st == st_begin ? 1u : 0u;
+#pragma unroll
+                        for (int sa = 1; sa <= kOzSMax; ++sa)
+#pragma unroll
+                            for (int sbk = 1; sbk <= kOzSMax; ++sbk) {
+                                const int w = sa + sbk;
+                                if (w < wlo || w > whi) continue;
+                                const uint32_t dt = tmem + (uint32_t)((w - wlo) * kOz2BN);
+                                const uint64_t da = dS + (uint64_t)(((sa - 1) * kOz2Slice) >> 4);
+                                const uint64_t db = dS + (uint64_t)(((kOzSMax + sbk - 1) * kOz2Slice) >> 4);
+                                // the first product of each weight in a round overwrites its accumulator
+                                const uint32_t accum = (sa == 1) ? (first ^ 1u) : 1u;
+                                asm volatile(
+                                    "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(dt),
+                                    "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                            }
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            oz_smem(&empty[sb])));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        oz_smem(&acc_full)));
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 0-7)
+        const int quarter = warp & 3, half = warp >> 2;
+        double acc[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+        int rglob = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            const int wlo = pass == 0 ? 2 : 6, whi = pass == 0 ? 5 : kOzSMax + 1;
+            for (int rd = 0; rd < nround; ++rd, ++rglob) {
+                oz_mbar_wait_sleep(&acc_full, (uint32_t)(rglob & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t lane_addr = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(64 * half);
+                for (int w = wlo; w <= whi; ++w) {   // fixed order
+                    const double sc = ldexp(1.0, -7 * w);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        uint32_t v[32];
+                        oz_ld32(lane_addr + (uint32_t)((w - wlo) * kOz2BN + 32 * hh), v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) acc[32 * hh + c] = fma((double)(int32_t)v[c], sc, acc[32 * hh + c]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                oz_mbar_arrive(&acc_empty);
+            }
+        }
+        const int64_t i = i0 + 32 * quarter + lane;
+        if (i < a.M) {
+            const int ei = oz_exp(__longlong_as_double((long long)a.amax[i]));
+            double* crow = a.C + i * a.ldc;
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+                const int64_t j = j0 + 64 * half + c;
+                if (j >= a.N || (a.lower && j > i)) continue;
+                const int ej = oz_exp(__longlong_as_double((long long)a.bmax[j]));
+                double v = a.alpha * ldexp(acc[c], ei + ej);
+                if (a.beta != 0.0) v += a.beta * crow[j];
+                if (i == j) v += a.diag;
+                crow[j] = v;
+                if (a.mirror && j < i) a.C[j * a.ldc + i] = v;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+static bool oz_n128() {
+    static const bool on = [] { const char* e = getenv("BICADMM_OZ_N64"); return !(e && atoi(e) != 0); }();
+    return on;
+}
+
 // ----------------------------------------------------------------------------- host
 static int64_t oz_rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -406,37 +609,6 @@ size_t gemm_tc_scratch_bytes(int64_t M, int64_t N, int64_t K, bool same) {
 size_t gram_tc_scratch_bytes(int dtype, int64_t m, int64_t nj) {
     (void)dtype;
     return gemm_tc_scratch_bytes(nj, nj, m, true);
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn oz_encode() {
-    static EncodeTiledFn fn = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return (EncodeTiledFn) nullptr;
-        return (EncodeTiledFn)f;
-    }();
-    return fn;
-}
-
-// 2-D map over digits [S * Lp rows (digit, operand row)] x [Kp bytes (summed index)], box
-// {32 bytes, box_rows}, 32-byte swizzle (the UMMA K-major SWIZZLE_32B layout)
-static int oz_map(CUtensorMap* map, int8_t* sl, int64_t Lp, int64_t Kp, uint32_t box_rows) {
-    EncodeTiledFn enc = oz_encode();
-    if (!enc) return BICADMM_ERR_CUDA;
-    const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)(kOzSMax * Lp)};
-    const cuuint64_t strides[1] = {(cuuint64_t)Kp};
-    const cuuint32_t box[2] = {(cuuint32_t)kOzBK, box_rows};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, sl, dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? BICADMM_OK : BICADMM_ERR_CUDA;
 }
 
 bool gram_tc_enabled() {
@@ -483,9 +655,13 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
     unsigned long long* amax = reinterpret_cast<unsigned long long*>(base + off);
     unsigned long long* bmax = g.same ? amax : amax + Mp;
     static bool attr = false;
-    const size_t smem = kOzStages * kOzStageBytes + 1024;   // + alignment slack
+    const bool n128 = oz_n128();
+    const size_t smem = (n128 ? kOz2Stages * kOz2StageBytes : kOzStages * kOzStageBytes) + 1024;   // + alignment slack
     if (!attr) {
-        BIC_CUDA(cudaFuncSetAttribute(k_oz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        BIC_CUDA(cudaFuncSetAttribute(k_oz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kOzStages * kOzStageBytes + 1024)));
+        BIC_CUDA(cudaFuncSetAttribute(k_oz_mm128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kOz2Stages * kOz2StageBytes + 1024)));
         attr = true;
     }
     // per-row scales of both operands over the whole summed range
@@ -500,8 +676,10 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
             BIC_LAUNCHED();
         }
     }
-    const int64_t ntb = Mp / kOzBM, ntj = oz_rup(g.N, kOzBN) / kOzBN;
-    const int64_t tiles = g.lower ? ntb * (ntb + 1) : ntb * ntj;   // lower: sum over bi of (2 bi + 2)
+    const int64_t ntb = Mp / kOzBM;
+    const int64_t bn = n128 ? kOz2BN : kOzBN, ntj = oz_rup(g.N, bn) / bn;
+    // lower: sum over bi of (bi + 1) 128-wide or (2 bi + 2) 64-wide column tiles
+    const int64_t tiles = g.lower ? (n128 ? ntb * (ntb + 1) / 2 : ntb * (ntb + 1)) : ntb * ntj;
     for (int64_t r_begin = 0; r_begin < (g.K > 0 ? g.K : 1); r_begin += kOzRowChunk) {
         const int64_t rows = g.K - r_begin < kOzRowChunk ? g.K - r_begin : kOzRowChunk;
         const int64_t Kp = oz_rup(rows > 0 ? rows : 1, kOzBK);
@@ -515,17 +693,14 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
                 BIC_LAUNCHED();
             }
         }
-        CUtensorMap tmA, tmB;
-        int rc = oz_map(&tmA, da, Mp, Kp, kOzBM);
-        if (!rc) rc = oz_map(&tmB, db, Np, Kp, kOzBN);
-        if (rc) return rc;
         OzArgs oa{};
         oa.M = g.M; oa.N = g.N; oa.Mp = Mp; oa.Np = Np; oa.Kp = rows > 0 ? Kp : 0; oa.ntj = ntj;
         oa.lower = g.lower; oa.mirror = g.mirror; oa.k_lo = g.k_lo; oa.k_hi = g.k_hi;
-        oa.K = g.K; oa.r_begin = r_begin; oa.amax = amax; oa.bmax = bmax;
+        oa.K = g.K; oa.r_begin = r_begin; oa.amax = amax; oa.bmax = bmax; oa.da = da; oa.db = db;
         oa.alpha = g.alpha; oa.beta = r_begin > 0 ? 1.0 : g.beta; oa.diag = r_begin > 0 ? 0.0 : g.diag;
         oa.C = g.C; oa.ldc = g.ldc;
-        k_oz_mm<<<(unsigned)tiles, kOzThreads, smem, s>>>(tmA, tmB, oa);
+        if (n128) k_oz_mm128<<<(unsigned)tiles, kOz2Threads, smem, s>>>(oa);
+        else k_oz_mm<<<(unsigned)tiles, kOzThreads, smem, s>>>(oa);
         BIC_LAUNCHED();
     }
     return BICADMM_OK;

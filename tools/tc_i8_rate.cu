@@ -7,6 +7,7 @@
 //   mode 3: as 2 with the commit/wait slot protocol of k_oz_gram
 //   mode 4: 7 tcgen05.cp per stage only
 //   mode 5: all 7 cps of a stage first (slots 0..6 / 7..13 alternating; N=56 layout), then 28 MMAs
+//   mode 6: SS with N = 128 (4 accumulators), mode 7: SS with N = 256 (2 accumulators)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/tc_i8_rate.cu -o tools/tc_i8_rate
 #include <cstdint>
 #include <cstdio>
@@ -37,7 +38,7 @@ __global__ void k_rate(int iters, long long* out) {
     __shared__ __align__(8) uint64_t bar[9];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int e = tid; e < 7 * 192 * 32; e += blockDim.x) sm[e] = (int8_t)(e * 7);
+    for (int e = tid; e < 7 * 128 * 32 + 3 * 256 * 32; e += blockDim.x) sm[e] = (int8_t)(e * 7);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -49,7 +50,7 @@ __global__ void k_rate(int iters, long long* out) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_base;
-    constexpr int NN = MODE == 5 ? 56 : 64;
+    constexpr int NN = MODE == 5 ? 56 : MODE == 6 ? 128 : MODE == 7 ? 256 : 64;
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t s0 = smem_u32(sm);
     const uint64_t dA0 = desc_sw32(s0), dB0 = desc_sw32(s0 + 7 * 128 * 32);
@@ -57,6 +58,17 @@ __global__ void k_rate(int iters, long long* out) {
         const long long t0 = clock64();
         uint32_t grp = 0;
         for (int it = 0; it < iters; ++it) {
+            if (MODE >= 6) {
+#pragma unroll
+                for (int q = 0; q < 28; ++q) {
+                    const uint32_t dt = tmem + (uint32_t)((q % (512 / NN)) * NN);
+                    const uint64_t da = dA0 + (uint64_t)(((q % 7) * 4096) >> 4);
+                    const uint64_t db = desc_sw32(s0 + 7 * 128 * 32 - 7 * 128 * 32 + 4096 * 7 + 0) + (uint64_t)((((q % 3) * NN * 32)) >> 4);
+                    asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(dt), "l"(da), "l"(db),
+                                 "r"(idesc));
+                }
+                continue;
+            }
             if (MODE == 5) {
                 const uint32_t base = tmem + 7 * NN + 56 * (it & 1);
 #pragma unroll
@@ -118,7 +130,7 @@ __global__ void k_rate(int iters, long long* out) {
 
 template <int MODE>
 void run(long long* d, int iters) {
-    const int smem = 7 * 192 * 32 + 1024;
+    const int smem = 7 * 128 * 32 + 3 * 256 * 32 + 1024;
     cudaFuncSetAttribute(k_rate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_rate<MODE><<<148, 128, smem>>>(iters, d);
     cudaError_t e = cudaDeviceSynchronize();
@@ -139,6 +151,7 @@ int main() {
     run<2>(d, iters);
     run<3>(d, iters);
     run<4>(d, iters);
-    run<5>(d, iters);
+    run<6>(d, iters);
+    run<7>(d, iters);
     return 0;
 }
