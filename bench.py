@@ -190,7 +190,9 @@ def run_ours(args):
     nl = args.nodes
     N = nl * world
     n, m, C, M = args.n, args.m, args.C, args.M
-    cs = dg.block_partition(n, M)
+    # feature blocks start on 128-byte boundaries (16 FP64 columns): a block's row slice is
+    # then whole cache lines, no line shared by two blocks' kernels (C4: 7 x 2,512 + 2,416)
+    cs = dg.block_partition(n, M, align=int(os.environ.get("BENCH_BLOCK_ALIGN", "16")))
     P = dg.generate(nl, m, n, args.kappa, args.loss, C=C, seed=1000 + rank, device="cuda", dtype=dtype)
     if n % 4:   # rows must start 16-byte aligned (lda % 4 == 0): pad the node matrices, one at a time
         for k in range(len(P.A)):

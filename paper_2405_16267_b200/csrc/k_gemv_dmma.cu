@@ -295,8 +295,17 @@ __global__ void __launch_bounds__(kGtdThreads, 2) k_gemv_t_dmma(const __grid_con
 // spending registers on it.  Rows are padded to 260 doubles: with the column mapping
 // g + 8j of the DMMA M-index, the 16 lanes of a half-warp read 4 rows x 32 contiguous
 // bytes each, 32 bytes apart modulo 128 (conflict-free).
-constexpr int kTtW = 256, kTtRS = 32, kTtLD = 260, kTtST = 3;
-constexpr int kTtThreads = 288;   // 8 consumer warps + 1 producer warp
+#ifndef BIC_TT_RS
+#define BIC_TT_RS 32
+#define BIC_TT_ST 3
+#endif
+constexpr int kTtW = 256, kTtRS = BIC_TT_RS, kTtLD = 260, kTtST = BIC_TT_ST;
+// 16 consumer warps: warp w takes the 32 columns 32 (w & 7) + g + 8j of the strip and the
+// row half w >> 3 of every stage (two independent accumulator sets per column, so twice
+// the DMMA chains in flight: with 8 warps the FP64 tensor pipe idled on the DMMA -> DMMA
+// dependency), summed in a fixed order (half 0 + half 1) at the end.
+constexpr int kTtCW = 16;
+constexpr int kTtThreads = 32 * kTtCW + 32;   // consumer warps + 1 producer warp
 constexpr size_t kTtSmem = sizeof(double) * (size_t)kTtST * kTtRS * (kTtLD + 2 * 16);
 
 __device__ __forceinline__ unsigned tt_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -341,25 +350,30 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTtST; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tt_smem(&full[s])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tt_smem(&empty[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tt_smem(&empty[s])), "r"(kTtCW));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == 8) {
-        if (lane == 0) {
-            const double* A = static_cast<const double*>(D.A);
-            for (int st = 0; st < nstage; ++st) {
-                const int s = st % kTtST;
+    if (warp == kTtCW) {
+        // all 32 lanes issue copies (lane i: row i; lane 0 also the p / delta slices): one
+        // thread issuing 34 bulk copies per stage was the stage-rate limit
+        const double* A = static_cast<const double*>(D.A);
+        for (int st = 0; st < nstage; ++st) {
+            const int s = st % kTtST;
+            const int64_t r0 = rb + (int64_t)st * kTtRS;
+            const int nr = (int)(re - r0 < kTtRS ? re - r0 : kTtRS);
+            const unsigned abytes = (unsigned)(wcols * 8), vbytes = (unsigned)(nr * C * 8);
+            if (lane == 0) {
                 if (st >= kTtST) tt_wait(&empty[s], (unsigned)((st / kTtST - 1) & 1));
-                const int64_t r0 = rb + (int64_t)st * kTtRS;
-                const int nr = (int)(re - r0 < kTtRS ? re - r0 : kTtRS);
-                const unsigned abytes = (unsigned)(wcols * 8), vbytes = (unsigned)(nr * C * 8);
                 const unsigned total = abytes * nr + vbytes * (D.delta ? 2u : 1u);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tt_smem(&full[s])),
                              "r"(total) : "memory");
-                double* as = As + (size_t)s * kTtRS * kTtLD;
-                for (int i = 0; i < nr; ++i) tt_bulk(as + i * kTtLD, A + (r0 + i) * D.lda + l0, abytes, &full[s]);
+            }
+            __syncwarp();
+            double* as = As + (size_t)s * kTtRS * kTtLD;
+            for (int i = lane; i < nr; i += 32) tt_bulk(as + i * kTtLD, A + (r0 + i) * D.lda + l0, abytes, &full[s]);
+            if (lane == 0) {
                 tt_bulk(Ps + (size_t)s * kTtRS * 16, D.p + r0 * C, vbytes, &full[s]);
                 if (D.delta) tt_bulk(Ds + (size_t)s * kTtRS * 16, D.delta + r0 * C, vbytes, &full[s]);
             }
@@ -372,7 +386,8 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
     for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[j][nt][0] = acc[j][nt][1] = 0.0;
-    const int cbase = 32 * warp + g;   // this thread's columns cbase + 8j
+    const int cbase = 32 * (warp & 7) + g;   // this thread's columns cbase + 8j
+    const int half = warp >> 3;               // rows [half RS/2, (half + 1) RS/2) of each stage
     for (int st = 0; st < nstage; ++st) {
         const int s = st % kTtST;
         tt_wait(&full[s], (unsigned)((st / kTtST) & 1));
@@ -382,8 +397,8 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
         const double* ps = Ps + (size_t)s * kTtRS * 16;
         const double* ds = Ds + (size_t)s * kTtRS * 16;
 #pragma unroll
-        for (int u = 0; u < kTtRS / 4; ++u) {
-            const int i = 4 * u + t;
+        for (int uu = 0; uu < kTtRS / 8; ++uu) {
+            const int i = 4 * (half * (kTtRS / 8) + uu) + t;
             const bool ok = i < nr;
             double a[4], q[NT];
 #pragma unroll
@@ -405,6 +420,21 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
         if (lane == 0) asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(
                                         tt_smem(&empty[s])) : "memory");
     }
+    // fixed-order sum of the two row halves through shared memory (the ring is drained: every
+    // stage was consumed by all consumer warps before they reach this barrier)
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTtCW) : "memory");
+    double* red = As + (size_t)(threadIdx.x & 255) * (4 * NT * 2);
+    if (half == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                red[(j * NT + nt) * 2] = acc[j][nt][0];
+                red[(j * NT + nt) * 2 + 1] = acc[j][nt][1];
+            }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTtCW) : "memory");
+    if (half == 1) return;
     // D[g][2t+e] of DMMA j: column l0 + 32 warp + g + 8j, class nt*8 + 2t + e
     double* out = D.partial + chunk * cols * C;
 #pragma unroll
@@ -417,7 +447,7 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int k = nt * 8 + 2 * t + e;
-                if (k < C) out[l * C + k] = acc[j][nt][e];
+                if (k < C) out[l * C + k] = acc[j][nt][e] + red[(j * NT + nt) * 2 + e];
             }
     }
 }

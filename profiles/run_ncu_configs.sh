@@ -15,6 +15,13 @@ run() {   # name, kernel regex, launch skip, bench args
       -o "$OUT/prof_$name" $CMD > "$OUT/ncu_$name.log" 2>&1
   echo "$name ncu rc=$?"
 }
-run c4 'k_gemv_t_dmma|k_gemv_dmma' 4 --config C4
+ONLY=${ONLY:-c4t c4 c3s c5s}
+for cfg in $ONLY; do case $cfg in
+  c4t) run c4t 'k_gemv_t_dmma' 1 --config C4 ;;
+  c4) run c4 'k_gemv_dmma' 4 --config C4 ;;
+  c3s) run c3s 'k_gemv_t_partial|k_gemv<' 4 --config C3s ;;
+  c5s) run c5s 'k_fused4' 2 --config C5s ;;
+esac; done
+exit 0
 run c3s 'k_gemv_t_partial|k_gemv<' 4 --config C3s
 run c5s 'k_fused4' 2 --config C5s
