@@ -451,7 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
     cluster_sync_all();   // no CTA exits while its peer may still write into its smem
 }
 
-int fused4_max_cols(int dtype) { return dtype == BICADMM_F64 ? 2 * kF4MainT * 16 : 2 * kF4MainT * 16; }
+int fused4_max_cols(int dtype) { (void)dtype; return 2 * kF4MainT * 17; }
 
 static size_t f4_slot_bytes(const Fused2Args& a, size_t es) { return (size_t)(((a.max_cols_pad / 2 + 3) / 4) * 4 + 4) * es; }
 static int f4_ring(const Fused2Args& a, size_t es) {
@@ -480,13 +480,15 @@ int fused4_groups(int dtype, int64_t max_cols) {
 }
 
 // axpy delay D (in the group's own rows; the ring holds about ngrp (D + 1) rows):
-// one group: D = 2 (measured best at C2 FP64; BICADMM_F4_D overrides); ngrp > 1: the
-// largest D that leaves 2 slots loading.  Always ngrp * D <= nring - 2.
+// one group: D = 2 (measured best at C2 FP64, 5 slots; BICADMM_F4_D overrides) but at
+// most nring - 3, so 2 slots keep loading (C3 shard, 4 slots of 50 KB: D = 1 runs at
+// 6.15 TB/s, D = 2 at 5.87); ngrp > 1: the largest D that leaves 2 slots loading.
 static int f4_delay(int nring, int ngrp) {
     static int d = [] { const char* e = getenv("BICADMM_F4_D"); return e ? (atoi(e) < 1 ? 1 : atoi(e)) : 0; }();
     int v = d ? d : (ngrp == 1 ? kF4D : (nring - 2) / ngrp - 1);
     if (v < 1) v = 1;
     while (v > 1 && ngrp * v > nring - 2) --v;
+    if (!d && ngrp == 1 && v > nring - 3) v = nring - 3 < 1 ? 1 : nring - 3;
     return v;
 }
 
@@ -508,7 +510,7 @@ static int f4_launch(int E, int ngrp, const Fused2Args& a, int loss, double rho,
         break;                                                                                                 \
     }
     switch (E) {
-        F4_CASE(2) F4_CASE(4) F4_CASE(8) F4_CASE(12) F4_CASE(14) F4_CASE(16)
+        F4_CASE(2) F4_CASE(4) F4_CASE(8) F4_CASE(12) F4_CASE(14) F4_CASE(16) F4_CASE(17)
     default: return BICADMM_ERR_INVALID;
     }
 #undef F4_CASE
@@ -522,7 +524,7 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     const int ngrp = fused4_groups(dtype, maxc);
     const int64_t gt = 32 * (kF4Main / ngrp);
     const int64_t e = (half + gt - 1) / gt;
-    const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 14 ? 14 : e <= 16 ? 16 : -1;
+    const int E = e <= 2 ? 2 : e <= 4 ? 4 : e <= 8 ? 8 : e <= 12 ? 12 : e <= 14 ? 14 : e <= 16 ? 16 : e <= 17 ? 17 : -1;
     if (E < 0 || f4_ring(a, dtype == BICADMM_F64 ? 8 : 4) < 4 || (grid & 1)) return BICADMM_ERR_INVALID;
     // TMA bulk copies: both half-rows start 16-byte aligned (ch % 4 == 0, lda * size % 16 == 0)
     // and are whole 16-byte multiples

@@ -389,6 +389,30 @@ def test_fused4_ragged_width(bc, orc):
         del os.environ["BICADMM_FUSED_KIND"]
 
 
+@pytest.mark.parametrize("loss", ["ls", "hinge"])
+def test_fused4_widest_rows_e17(bc, loss):
+    # n_j = 12,500 FP64 (the C3 shard's block width: 50 KB half-rows, a 4-slot ring, 17
+    # elements per lane, axpy delay 1): the auto-chosen single-pass kernel against the
+    # independent two-pass kernels, iterate by iterate (1e-9)
+    P = dg.generate(1, 12_600, 12_500, 20, loss, seed=17, device="cuda")   # tall: m_i >= n_j
+    cs = dg.block_partition(12_500, 1)
+    prm = dict(kappa=20, max_outer=4, inner_fixed=3, eps_p=0.0, eps_d=0.0, eps_b=0.0, refit=0)
+    out = {}
+    for sweep in (0, 1):
+        s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], loss, bc.Params(sweep=sweep, **prm), cs)
+        if sweep == 0:
+            assert s.sweep_kind() == (4, 0)
+        zs = []
+        for _ in range(4):
+            s.iterate(1)
+            zs.append(s.z)
+        out[sweep] = (np.array(zs), s.get(bc.FIELD_X_LOCAL))
+        s.close()
+    for k in range(4):
+        assert _rel(out[0][0][k], out[1][0][k]) <= 1e-9, k
+    assert _rel(out[0][1], out[1][1]) <= 1e-9
+
+
 def test_auto_sweep_choice(bc):
     # sweep = 0: the CTA-pair single-pass kernel for rows >= 24 KB (C = 1, single-block
     # nodes), two-pass otherwise
