@@ -31,7 +31,7 @@ constexpr int kF4Main = 12;                    // main warps per CTA
 constexpr int kF4Prox = 3;                     // prox warps per CTA
 constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp = 512
 constexpr int kF4MainT = 32 * kF4Main;         // 384
-constexpr int kF4RingMax = 16;                 // half-row ring depth (runtime nring <= 16, by smem)
+constexpr int kF4RingMax = 32;                 // half-row ring depth (runtime nring <= 32 = kF4Q, by smem)
 constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
 constexpr int kF4Q = 32;                       // dot / q slots (>= delay + lag window)
 
@@ -177,12 +177,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
     // row groups: the 12 main warps form ngrp groups of W warps; group gi owns the
     // rows rb + gi, rb + gi + ngrp, ...  For narrow rows this overlaps the per-row latency
     // chain of ngrp rows.  Every row's dot has W partials per CTA.
-    if (GR == 1) ngrp = 1;               // GR = 1: one group, W = 12 at compile time
+    ngrp = GR;                           // GR groups of W = 12 / GR warps, fixed at compile time
     const int W = kF4Main / ngrp;
     extern __shared__ __align__(128) unsigned char f4_smem[];
     T* ring = reinterpret_cast<T*>(f4_smem);             // nring x half_pad elements
     __shared__ double dotp[kF4Q][2 * kF4Main];            // [slot][cta * 12 + warp]
     __shared__ double qv[kF4Q];
+    __shared__ double tok[kF4Q];                          // CTA 1 -> CTA 0: row inputs read
     __shared__ __align__(8) uint64_t bar_full[kF4RingMax], bar_empty[kF4RingMax], bar_dot[kF4Q], bar_q[kF4Q];
     const unsigned h = cluster_rank();                     // column half owned by this CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                                  &bar_full[s]);
             }
         }
-    } else if (GR == 0 && warp < kF4Main) {
+    } else if (GR != 1 && warp < kF4Main) {
         // ------------------------------------------------------------ main warps (row groups)
         const int gi = warp / W, wig = warp % W;
         const int GT = 32 * W;                 // threads of a group (cover a half-row)
@@ -297,7 +298,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                     const int idx = (int)h * W + wig;
                     dotp[q][idx] = dot;
                     st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
-                    if (wig == 0) mb4_expect_tx(&bar_dot[q], 8u * W);   // the peer group's W stores
+                    // the peer group's W stores (+ on CTA 0 the peer's "inputs read" token)
+                    if (wig == 0) mb4_expect_tx(&bar_dot[q], 8u * (W + (h == 0 ? 1 : 0)));
                     else mb4_arrive_local(&bar_dot[q]);
                 }
             }
@@ -379,7 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                     const int idx = (int)h * kF4Main + warp;
                     dotp[q][idx] = dot;
                     st_async_f64(mapa(smem_u32(&dotp[q][idx]), peer), dot, mapa(smem_u32(&bar_dot[q]), peer));
-                    if (warp == 0) mb4_expect_tx(&bar_dot[q], 8u * kF4Main);   // the peer's 12 stores
+                    // the peer's 12 stores (+ on CTA 0 the peer's "inputs read" token)
+                    if (warp == 0) mb4_expect_tx(&bar_dot[q], 8u * (kF4Main + (h == 0 ? 1 : 0)));
                     else mb4_arrive_local(&bar_dot[q]);
                 }
             }
@@ -412,41 +415,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         if (a.active[nda]) flush(nda);
     } else if (lane == 0) {
         // ------------------------------------------------------------ prox warps (lane 0)
+        // The per-sample inputs (b, nu, delta, p) of a warp's next row are loaded while it
+        // waits for the current row's dots (their global-load latency is ~1 us, several row
+        // periods when rows are narrow).
         const int pw = warp - kF4Main;
         int nd = nd0;
-        for (int64_t r = rb + pw; r < re; r += kF4Prox) {
-            nd = node_of(r, nd);
-            const int q = (int)((r - rb) % kF4Q);
-            const int64_t rl = r - a.row_off[nd];
-            const bool on = a.active[nd];
-            double bl = 0.0, nu0 = 0.0, w0 = 0.0;
-            if (on) {
-                bl = (double)static_cast<const T*>(a.b[nd])[rl];
-                nu0 = a.nu[nd][rl];
-                w0 = a.delta[nd][rl] + a.p[nd][rl] + nu0;
+        struct In { int nd; int64_t rl; bool on; double bl, nu0, w0; };
+        auto fetch = [&](int64_t r, int from) {
+            In v;
+            v.nd = node_of(r, from);
+            v.rl = r - a.row_off[v.nd];
+            v.on = a.active[v.nd];
+            v.bl = v.nu0 = v.w0 = 0.0;
+            if (v.on) {
+                v.bl = (double)static_cast<const T*>(a.b[v.nd])[v.rl];
+                v.nu0 = a.nu[v.nd][v.rl];
+                v.w0 = a.delta[v.nd][v.rl] + a.p[v.nd][v.rl] + v.nu0;
             }
+            return v;
+        };
+        // CTA 0 overwrites p, nu, delta of a row once it has both CTAs' dots; CTA 1 reads the
+        // same entries.  CTA 1 therefore sends a token, data-dependent on its loaded values, that
+        // completes 8 bytes of CTA 0's dot barrier for that row: CTA 0 cannot write a row before
+        // CTA 1 has read it.
+        auto token = [&](int64_t r, const In& v) {
+            if (h == 1) {
+                const int qt = (int)((r - rb) % kF4Q);
+                st_async_f64(mapa(smem_u32(&tok[qt]), 0u), v.on ? v.w0 + v.bl : 0.0, mapa(smem_u32(&bar_dot[qt]), 0u));
+            }
+        };
+        In cur = fetch(rb + pw < re ? rb + pw : rb, nd);
+        if (rb + pw < re) token(rb + pw, cur);
+        for (int64_t r = rb + pw; r < re; r += kF4Prox) {
+            In nxt = cur;
+            if (r + kF4Prox < re) {
+                nxt = fetch(r + kF4Prox, cur.nd);
+                token(r + kF4Prox, nxt);
+            }
+            const int q = (int)((r - rb) % kF4Q);
             // the peer's dots arrive by st.async complete_tx on this CTA's barrier: observing the
             // phase (CTA-scope acquire, as for TMA) makes them visible; no cluster-scope acquire
             mb4_wait_cta(&bar_dot[q], (unsigned)(((r - rb) / kF4Q) & 1));
             double qq = 0.0;
-            if (on) {
+            if (cur.on) {
                 double p = 0.0;
 #pragma unroll
                 for (int w = 0; w < 2 * W; ++w) p += dotp[q][w];
-                const double om = f4_prox(loss, rho, bl, p + nu0, w0);
-                const double nu = nu0 + p - om;
+                const double om = f4_prox(loss, rho, cur.bl, p + cur.nu0, cur.w0);
+                const double nu = cur.nu0 + p - om;
                 const double dl = om - p - nu;
                 if (h == 0) {
-                    a.p[nd][rl] = p;
-                    a.nu[nd][rl] = nu;
-                    a.delta[nd][rl] = dl;
-                    if (a.e2row[nd]) a.e2row[nd][rl] = (p - om) * (p - om);
+                    a.p[cur.nd][cur.rl] = p;
+                    a.nu[cur.nd][cur.rl] = nu;
+                    a.delta[cur.nd][cur.rl] = dl;
+                    if (a.e2row[cur.nd]) a.e2row[cur.nd][cur.rl] = (p - om) * (p - om);
                 }
                 qq = p + dl;
             }
             qv[q] = qq;
             mb4_arrive_local(&bar_q[q]);
+            cur = nxt;
         }
+        (void)nd;
     }
     cluster_sync_all();   // no CTA exits while its peer may still write into its smem
 }
@@ -462,19 +492,20 @@ static int f4_ring(const Fused2Args& a, size_t es) {
 }
 
 // Row groups for narrow rows: the largest ngrp in {6, 4, 3, 2} whose W = 12/ngrp warps
-// still cover a half-row with <= 12 elements per thread (BICADMM_F4_GROUPS overrides,
-// up to 16 elements).  Measured at n = 4000 FP64: 1 group 3.30 ms, 2 groups 2.49 ms,
-// 3 groups (E = 16) 2.86 ms per sweep.
+// still cover a half-row with <= 17 elements per thread (every group count is compiled
+// with W fixed: no spills up to E = 17; BICADMM_F4_GROUPS overrides).  Measured: n = 4000
+// FP64 (Table-1 rows) 3 groups 1.87 ms per sweep vs 2 groups 2.05 ms (2.44 ms with the
+// runtime-W kernel); C5 shard (n_j = 6,250) 2 groups 17.7 ms vs 1 group 23.9 ms.
 int fused4_groups(int dtype, int64_t max_cols) {
     (void)dtype;
     const int64_t half = (max_cols + 1) / 2 + 2;
     int g = 1;
     const int cand[4] = {6, 4, 3, 2};
-    for (int k = 0; k < 4; ++k)   // E <= 12 (E = 16 with runtime W spills; measured)
-        if (half <= (int64_t)32 * (kF4Main / cand[k]) * 12) { g = cand[k]; break; }
+    for (int k = 0; k < 4; ++k)
+        if (half <= (int64_t)32 * (kF4Main / cand[k]) * 17) { g = cand[k]; break; }
     if (const char* e = getenv("BICADMM_F4_GROUPS")) {
         const int v = atoi(e);
-        if (v >= 1 && kF4Main % v == 0 && half <= (int64_t)32 * (kF4Main / v) * 16) g = v;
+        if ((v == 1 || v == 2 || v == 3 || v == 4 || v == 6) && half <= (int64_t)32 * (kF4Main / v) * 17) g = v;
     }
     return g;
 }
@@ -482,10 +513,12 @@ int fused4_groups(int dtype, int64_t max_cols) {
 // axpy delay D (in the group's own rows; the ring holds about ngrp (D + 1) rows):
 // one group: D = 2 (measured best at C2 FP64, 5 slots; BICADMM_F4_D overrides) but at
 // most nring - 3, so 2 slots keep loading (C3 shard, 4 slots of 50 KB: D = 1 runs at
-// 6.15 TB/s, D = 2 at 5.87); ngrp > 1: the largest D that leaves 2 slots loading.
+// 6.15 TB/s, D = 2 at 5.87).  Always ngrp * D <= nring - 2.
 static int f4_delay(int nring, int ngrp) {
     static int d = [] { const char* e = getenv("BICADMM_F4_D"); return e ? (atoi(e) < 1 ? 1 : atoi(e)) : 0; }();
-    int v = d ? d : (ngrp == 1 ? kF4D : (nring - 2) / ngrp - 1);
+    // ngrp > 1: D = 1 (a group's next row comes ngrp rows later, so the prox chain already
+    // has ngrp row periods), which keeps the most slots loading
+    int v = d ? d : (ngrp == 1 ? kF4D : 1);
     if (v < 1) v = 1;
     while (v > 1 && ngrp * v > nring - 2) --v;
     if (!d && ngrp == 1 && v > nring - 3) v = nring - 3 < 1 ? 1 : nring - 3;
@@ -531,10 +564,17 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     const int64_t es = dtype == BICADMM_F64 ? 8 : 4;
     for (int k = 0; k < a.nn; ++k) if ((a.ncols[k] * es) % 16 || (a.lda[k] * es) % 16) return BICADMM_ERR_INVALID;
     int rc;
-    if (dtype == BICADMM_F64)
-        rc = ngrp == 1 ? f4_launch<double, 1>(E, 1, a, loss, rho, grid, s) : f4_launch<double, 0>(E, ngrp, a, loss, rho, grid, s);
-    else
-        rc = ngrp == 1 ? f4_launch<float, 1>(E, 1, a, loss, rho, grid, s) : f4_launch<float, 0>(E, ngrp, a, loss, rho, grid, s);
+#define F4_GROUPS(TT)                                                                  \
+    switch (ngrp) {                                                                    \
+    case 1: rc = f4_launch<TT, 1>(E, 1, a, loss, rho, grid, s); break;                 \
+    case 2: rc = f4_launch<TT, 2>(E, 2, a, loss, rho, grid, s); break;                 \
+    case 3: rc = f4_launch<TT, 3>(E, 3, a, loss, rho, grid, s); break;                 \
+    case 4: rc = f4_launch<TT, 4>(E, 4, a, loss, rho, grid, s); break;                 \
+    case 6: rc = f4_launch<TT, 6>(E, 6, a, loss, rho, grid, s); break;                 \
+    default: rc = BICADMM_ERR_INVALID;                                                 \
+    }
+    if (dtype == BICADMM_F64) { F4_GROUPS(double) } else { F4_GROUPS(float) }
+#undef F4_GROUPS
     if (rc) return rc;
     BIC_LAUNCHED();
     return BICADMM_OK;
