@@ -222,14 +222,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         cn = h == 0 ? ch : nc - ch;
     };
     const int nd0 = node_of(rb, 0);
+    // rows are visited in increasing order at every call site: keep the current node's end
+    // row in a register instead of re-scanning row_off (parameter space) for every row
+    struct NodeCur {
+        int nd;
+        int64_t end;
+    };
+    auto cur_init = [&](int nd) { return NodeCur{nd, nd + 1 < a.nn ? a.row_off[nd + 1] : INT64_MAX}; };
+    auto cur_adv = [&](NodeCur& c, int64_t r) {   // true when r starts another node
+        if (r < c.end) return false;
+        c = cur_init(node_of(r, c.nd));
+        return true;
+    };
 
     if (warp == kF4Main + kF4Prox) {
         // ------------------------------------------------------------ producer (lane 0)
         if (lane == 0) {
-            int nd = nd0;
+            NodeCur nc = cur_init(nd0);
             RingPos pw;
             for (int64_t r = rb; r < re; ++r, pw.next(nring)) {
-                nd = node_of(r, nd);
+                cur_adv(nc, r);
+                const int nd = nc.nd;
                 const int s = pw.s;
                 if (r - rb >= nring) mb4_wait_cta(&bar_empty[s], pw.ph ^ 1u);   // (w-1)-th release
                 int64_t c0, cn;
@@ -249,6 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         const int mt = wig * 32 + lane;
         const unsigned peer = h ^ 1u;
         int ndd = nd0, nda = nd0;
+        int64_t ndd_end = cur_init(nd0).end, nda_end = ndd_end;
         double xr[E], acc[E];
         int64_t hc0, hcn;
         auto load_x = [&](int nd) {
@@ -278,8 +292,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         const int64_t lag = (int64_t)D * ngrp;
         for (int64_t k = rb + gi; k < re + lag; k += ngrp) {
             if (k < re) {
-                const int nn2 = node_of(k, ndd);
-                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
+                if (k >= ndd_end) {
+                    ndd = node_of(k, ndd);
+                    ndd_end = cur_init(ndd).end;
+                    load_x(ndd);
+                }
                 const int s = pd.s;
                 mb4_wait_cta(&bar_full[s], pd.ph);
                 pd.adv(nring, ngrp);
@@ -305,10 +322,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             }
             const int64_t ra = k - lag;
             if (ra >= rb) {
-                const int nn2 = node_of(ra, nda);
-                if (nn2 != nda) {
+                if (ra >= nda_end) {
                     if (a.active[nda]) flush(nda);
-                    nda = nn2;
+                    nda = node_of(ra, nda);
+                    nda_end = cur_init(nda).end;
                     half_range(nda, ac0, acn);
                 }
                 const int q = (int)((ra - rb) % kF4Q);
@@ -334,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         const int mt = threadIdx.x;
         const unsigned peer = h ^ 1u;
         int ndd = nd0, nda = nd0;
+        int64_t ndd_end = cur_init(nd0).end, nda_end = ndd_end;
         double xr[E], acc[E];
         int64_t hc0, hcn;
         auto load_x = [&](int nd) {
@@ -361,8 +379,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         RingPos pd, pa;
         for (int64_t k = rb; k < re + D; ++k) {
             if (k < re) {
-                const int nn2 = node_of(k, ndd);
-                if (nn2 != ndd) { ndd = nn2; load_x(ndd); }
+                if (k >= ndd_end) {
+                    ndd = node_of(k, ndd);
+                    ndd_end = cur_init(ndd).end;
+                    load_x(ndd);
+                }
                 const int s = pd.s;
                 mb4_wait_cta(&bar_full[s], pd.ph);
                 pd.next(nring);
@@ -388,10 +409,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             }
             const int64_t ra = k - D;
             if (ra >= rb) {
-                const int nn2 = node_of(ra, nda);
-                if (nn2 != nda) {
+                if (ra >= nda_end) {
                     if (a.active[nda]) flush(nda);
-                    nda = nn2;
+                    nda = node_of(ra, nda);
+                    nda_end = cur_init(nda).end;
                     half_range(nda, ac0, acn);
                 }
                 const int q = (int)((ra - rb) % kF4Q);
@@ -421,9 +442,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         const int pw = warp - kF4Main;
         int nd = nd0;
         struct In { int nd; int64_t rl; bool on; double bl, nu0, w0; };
+        NodeCur pc = cur_init(nd0);
         auto fetch = [&](int64_t r, int from) {
+            (void)from;
             In v;
-            v.nd = node_of(r, from);
+            cur_adv(pc, r);
+            v.nd = pc.nd;
             v.rl = r - a.row_off[v.nd];
             v.on = a.active[v.nd];
             v.bl = v.nu0 = v.w0 = 0.0;

@@ -5,7 +5,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2405_16267_b200 import bicadmm as bc, datagen as dg
 
-n, m, N, sl = 4000, 300_000, 4, 0.9
+n, m, N, sl = int(os.environ.get("TTT_N", "4000")), 300_000, 4, 0.9
 kappa = int(round(n * (1 - sl)))
 P = dg.generate(N, m // N, n, kappa, "ls", seed=0, device="cuda")
 cs = dg.block_partition(n, 1)
