@@ -139,9 +139,10 @@ __device__ __forceinline__ bool mb4_try_cluster(uint64_t* b, unsigned parity) {
         : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
     return ok != 0;
 }
+// (a try_wait suspend-time hint of 1 or 20 us measured no better than plain polling)
 __device__ __forceinline__ void mb4_wait_cta(uint64_t* b, unsigned parity) {
-    for (long long it = 0; !mb4_try_cta(b, parity); ++it)
-        if (it > (1ll << 26)) asm volatile("trap;");
+    for (unsigned it = 0; !mb4_try_cta(b, parity);)
+        if (++it > (1u << 26)) asm volatile("trap;");
 }
 __device__ __forceinline__ void mb4_wait_cluster(uint64_t* b, unsigned parity) {
     for (long long it = 0; !mb4_try_cluster(b, parity); ++it)
