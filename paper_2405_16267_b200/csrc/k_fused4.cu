@@ -2,8 +2,9 @@
 //
 // Same algebra as the two-pass sweep (Eqs. (22)-(24)) for nodes with one local
 // block.  A cluster of 2 CTAs (2 SMs) owns a contiguous row range; CTA h of the pair
-// owns column half h of every row, so a 5-deep ring of half-rows fits in shared
-// memory even at n = 10^4 in FP64 (5 x 40 KB):
+// owns column half h of every row, so a ring of half-rows fits in shared memory even
+// for wide rows (up to 210 KB: 5 x 40 KB at n = 10^4 FP64, 4 x 50 KB at 12,500, up to
+// 32 slots for narrow rows):
 //
 //   producer warp : TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of a half-row
 //                   into the ring as soon as its slot is released
@@ -16,9 +17,11 @@
 //                   delta = omega - p - nu, q = p + delta; rank 0 stores p, nu, delta.
 //
 // Both CTAs compute the prox redundantly from bit-identical inputs, so the only
-// cluster traffic per row is 12 doubles each way.  A crosses HBM exactly once per
-// sweep; partial products are written per (cluster, row group) and reduced in fixed
-// order by the next sweep's Eq. (24) epilogue (bit-reproducible).
+// cluster traffic per row is 12 doubles each way plus one 8-byte token from CTA 1 (it
+// has read the row's p, nu, delta, which only CTA 0 overwrites).  Narrow rows run as
+// 2, 3, 4 or 6 row groups of 12/g main warps (compiled per g).  A crosses HBM exactly
+// once per sweep; partial products are written per (cluster, row group) and reduced in
+// fixed order by the next sweep's Eq. (24) epilogue (bit-reproducible).
 #include <cfloat>
 #include <stdlib.h>
 

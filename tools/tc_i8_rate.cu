@@ -4,7 +4,7 @@
 //   mode 1: A from TMEM (fixed slot), B from smem (TS), no copies
 //   mode 2: TS with one tcgen05.cp 128x256b per slice group (7 per stage), single slot per
 //           group rotating over 8 slots, no waits
-//   mode 3: as 2 with the commit/wait slot protocol of k_oz_gram
+//   mode 3: as 2 with the commit/wait slot protocol of an A-in-TMEM Ozaki kernel (measured, not adopted)
 //   mode 4: 7 tcgen05.cp per stage only
 //   mode 5: all 7 cps of a stage first (slots 0..6 / 7..13 alternating; N=56 layout), then 28 MMAs
 //   mode 6: SS with N = 128 (4 accumulators), mode 7: SS with N = 256 (2 accumulators)

@@ -2,7 +2,7 @@
 // tcgen05.mma kind::i8 with A from TMEM and B from smem (M=128, N=64, K=32), both smem
 // tiles in the SWIZZLE_32B K-major layout (32-byte rows, 16-byte chunk index ^= row bit 2).
 // Also: two K chunks accumulated, the second A copied into a different TMEM slot after
-// the first MMA was committed (the slot-rotation pattern of k_oz_gram).
+// the first MMA was committed (the slot-rotation pattern tried for the Ozaki kernel).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/tc_i8_ts_test.cu -o tools/tc_i8_ts_test
 #include <cstdint>
 #include <cstdio>
