@@ -883,12 +883,13 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             // auto: the CTA-pair single-pass sweep (k_fused4) where eligible -- measured on B200
             // (profiles/r01_summary.md) 1.45 ms vs 2.43 ms for the two HBM passes on configs[1];
             // kinds 1-3 are slower than the two-pass sweep, which is taken otherwise
-            // rows narrower than 24 KB leave the single-pass kernel latency-bound per row
-            // (Table-1 shapes: n = 4000 FP64 2.44 ms fused vs 3.0 two-pass; n = 2000 1.75 vs ~1.5)
+            // rows narrower than 14 KB leave the single-pass kernel bound by its per-row chain
+            // (Table-1 shape, 300k rows, solve time: n = 1500 FP64 520 ms fused vs 496 two-pass;
+            // n = 2000 535 vs 609; n = 3000 573 vs 878)
             int64_t maxc = 0;
             for (auto& L : h->blk) maxc = std::max(maxc, L.nj);
             const int64_t row_bytes = maxc * (P->dtype == BICADMM_F64 ? 8 : 4);
-            kind = ok4 && row_bytes >= 24576 ? 4 : 0;
+            kind = ok4 && row_bytes >= 14336 ? 4 : 0;
         }
         if (fk && kind != 0) {
             const int want = atoi(fk);
