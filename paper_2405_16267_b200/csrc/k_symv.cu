@@ -119,32 +119,47 @@ __global__ void __launch_bounds__(kSymvThreads) k_symv_tiles(const SymvBatch B) 
 }
 
 // y[r] = alpha * (sum_{J <= I} part[(I, J)][0][rr] + sum_{K > I} part[(K, I)][1][rr])
-__global__ void __launch_bounds__(256) k_symv_reduce(const SymvBatch B) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= B.elem_begin[B.nd]) return;
-    int k = 0;
-    while (k + 1 < B.nd && e >= B.elem_begin[k + 1]) ++k;
-    const SymvDesc& D = B.d[k];
-    const int64_t r = e - B.elem_begin[k];
-    const int64_t I = r / kTS, rr = r % kTS, nb = (D.n + kTS - 1) / kTS;
-    const double* P = D.part;
-    // the (nb) terms in a fixed order: J = 0..I (row dots of tile (I, J)), then
-    // K = I+1..nb-1 (column dots of tile (K, I)); loads issued 8 at a time ahead of the adds
-    const int64_t row0 = I * (I + 1) / 2;
-    auto addr = [&](int64_t q) -> const double* {
-        return q <= I ? P + (row0 + q) * (2 * kTS) + rr : P + (q * (q + 1) / 2 + I) * (2 * kTS) + kTS + rr;
-    };
+// CTA = 64 outputs x 4 sub-ranges of the nb terms (4x the loads in flight of one thread
+// per output: the sum is latency-bound); the 4 sub-sums are added in a fixed order.
+constexpr int kRedOut = 64, kRedSub = 4;
+__global__ void __launch_bounds__(kRedOut * kRedSub) k_symv_reduce(const SymvBatch B) {
+    __shared__ double part_s[kRedSub][kRedOut];
+    const int o = threadIdx.x % kRedOut, sub = threadIdx.x / kRedOut;
+    const int64_t e = (int64_t)blockIdx.x * kRedOut + o;
+    const bool live = e < B.elem_begin[B.nd];
     double s = 0.0;
-    int64_t q = 0;
-    for (; q + 8 <= nb; q += 8) {
-        double v[8];
+    int k = 0;
+    int64_t r = 0;
+    if (live) {
+        while (k + 1 < B.nd && e >= B.elem_begin[k + 1]) ++k;
+        const SymvDesc& D = B.d[k];
+        r = e - B.elem_begin[k];
+        const int64_t I = r / kTS, rr = r % kTS, nb = (D.n + kTS - 1) / kTS;
+        const double* P = D.part;
+        // the nb terms in a fixed order: J = 0..I (row dots of tile (I, J)), then
+        // K = I+1..nb-1 (column dots of tile (K, I)); this thread's contiguous quarter,
+        // loads issued 8 at a time ahead of the adds
+        const int64_t row0 = I * (I + 1) / 2;
+        auto addr = [&](int64_t q) -> const double* {
+            return q <= I ? P + (row0 + q) * (2 * kTS) + rr : P + (q * (q + 1) / 2 + I) * (2 * kTS) + kTS + rr;
+        };
+        const int64_t q0 = nb * sub / kRedSub, q1 = nb * (sub + 1) / kRedSub;
+        int64_t q = q0;
+        for (; q + 8 <= q1; q += 8) {
+            double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(addr(q + u));
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(addr(q + u));
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; q < q1; ++q) s += __ldcg(addr(q));
     }
-    for (; q < nb; ++q) s += __ldcg(addr(q));
-    D.y[r] = D.alpha * s;
+    part_s[sub][o] = s;
+    __syncthreads();
+    if (sub == 0 && live) {
+        const double t = ((part_s[0][o] + part_s[1][o]) + part_s[2][o]) + part_s[3][o];
+        B.d[k].y[r] = B.d[k].alpha * t;
+    }
 }
 
 int launch_symv_packed(int dtype, const SymvDesc* d, int nd, cudaStream_t s) {
@@ -166,7 +181,7 @@ int launch_symv_packed(int dtype, const SymvDesc* d, int nd, cudaStream_t s) {
         if (dtype == BICADMM_F64) k_symv_tiles<double><<<(unsigned)t, kSymvThreads, 0, s>>>(B);
         else k_symv_tiles<float><<<(unsigned)t, kSymvThreads, 0, s>>>(B);
         BIC_LAUNCHED();
-        k_symv_reduce<<<(unsigned)((e + 255) / 256), 256, 0, s>>>(B);
+        k_symv_reduce<<<(unsigned)((e + kRedOut - 1) / kRedOut), kRedOut * kRedSub, 0, s>>>(B);
         BIC_LAUNCHED();
     }
     return BICADMM_OK;
