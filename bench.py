@@ -284,7 +284,8 @@ def run_ours(args):
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(args.config, {}).get(dom, {}).get("bytes_per_launch")
+        key = args.config if args.dtype == "f64" else f"{args.config}/{args.dtype}"
+        traffic = tr.get(key, {}).get(dom, {}).get("bytes_per_launch")
     except Exception:
         pass
     fused_mode = phases["fused_sweep"][1] > 0
