@@ -88,3 +88,31 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not bad.search(src), f
+
+
+def test_ctypes_struct_layout_matches_header(tmp_path):
+    # the binding's ctypes structs against the C header: size and every field offset, read
+    # from a tiny gcc-compiled program (a drifted field would silently corrupt the ABI)
+    import ctypes as ct
+    import subprocess
+    from paper_2405_16267_b200 import bicadmm as bc
+    structs = [bc.bicadmm_block, bc.bicadmm_problem, bc.bicadmm_params, bc.bicadmm_step_info, bc.bicadmm_report]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "bicadmm.h"', 'int main(void) {']
+    for S in structs:
+        name = S.__name__
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for f in S._fields_:   # ctypes names a C field `lambda` as `lambda_`
+            lines.append(f'printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0].rstrip("_")}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for S in structs:
+        name = S.__name__
+        assert got[(name, "size")] == ct.sizeof(S), name
+        for f in S._fields_:
+            assert got[(name, f[0])] == getattr(S, f[0]).offset, (name, f[0])
