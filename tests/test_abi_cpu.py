@@ -116,3 +116,26 @@ def test_ctypes_struct_layout_matches_header(tmp_path):
         assert got[(name, "size")] == ct.sizeof(S), name
         for f in S._fields_:
             assert got[(name, f[0])] == getattr(S, f[0]).offset, (name, f[0])
+
+
+def test_binding_argument_counts_match_prototypes():
+    # every prototype in include/*.h against the binding's argtypes (count per function)
+    import ctypes as ct
+    from paper_2405_16267_b200 import bicadmm as bc
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    protos = {}
+    for h in ("bicadmm.h", "bicadmm_ops.h"):
+        text = open(os.path.join(root, "include", h)).read()
+        text = re.sub(r"/\*.*?\*/", " ", text, flags=re.S)
+        for m in re.finditer(r"\b(bicadmm_\w+)\s*\(([^;{]*?)\)\s*;", text):
+            args = m.group(2).strip()
+            protos[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    L = bc.lib()
+    checked = 0
+    for name, n in protos.items():
+        f = getattr(L, name, None)
+        if f is None or f.argtypes is None:
+            continue
+        assert len(f.argtypes) == n, (name, len(f.argtypes), n)
+        checked += 1
+    assert checked >= 20, checked
