@@ -331,7 +331,7 @@ def run_ours(args):
                 b_all2[rank * nl + k] = db[k]
                 for j in range(M):
                     blocks2.append((rank * nl + k, j, dA[k][:, cs[j]:cs[j + 1]], evs[k]))
-            s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, check_domain=False, C=C)
+            s2 = bc.BiCADMM(None, b_all2, args.loss, prm, cs, blocks=blocks2, comm=comm, C=C)
             for _ in range(args.steps):
                 s2.iterate(1)          # each step reads back its 6 residual scalars
             z = s2.z                   # D2H of the result

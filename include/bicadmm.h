@@ -165,8 +165,8 @@ typedef enum {
                                     profiling is on (CUDA events on the handle's stream) */
     BICADMM_FIELD_PHASE_COUNT = 13, /* int64 [BICADMM_NPHASE]: kernel launches per phase while profiling */
     BICADMM_FIELD_SWEEP_KIND = 14, /* int32 [2]: inner-sweep implementation chosen at setup (0 two-pass,
-                                     1-4 single-pass kernels k_fused, k_fused2, k_fused3, k_fused4) and
-                                     the number of local Woodbury (fat) blocks */
+                                     4 the CTA-pair single-pass kernel k_fused4) and the number of local
+                                     Woodbury (fat) blocks */
     BICADMM_FIELD_P_LOCAL = 15,  /* per local block in blocks[] order: p_ij = A_ij x_ij of the last sweep
                                     (m_i*C each, concatenated; property checks at full size) */
     BICADMM_FIELD_R_LOCAL = 16   /* per local block: r_ij = rho_l A_ij^T q + rho_c (z_j - u_ij) of the last
@@ -193,11 +193,32 @@ const char* bicadmm_rc_string(int rc);
  * share a color; the per-sweep m-vector AllReduce (Algorithm 2) runs over
  * that group, the per-outer n-vector AllReduce ("Collect") over all ranks.
  * NCCL is loaded at run time (libnccl.so.2); world == 1 needs no NCCL and a NULL
- * comm passed to bicadmm_setup means a single rank. */
+ * comm passed to bicadmm_setup means a single rank.  NCCL_ALGO / NCCL_PROTO are pinned
+ * to Ring / Simple unless the caller set them (run-to-run identical reduction order).
+ * bicadmm_setup on more than one rank is collective: it checks that every (node, block)
+ * pair is held by exactly one rank and that each node group holds all blocks of its
+ * nodes (else BICADMM_ERR_PLACEMENT on every rank). */
 int bicadmm_uid_size(void);
 int bicadmm_get_unique_id(void* uid_out);
 int bicadmm_comm_init(int world, int rank, int device, const void* uid, int group_color, bicadmm_comm** out);
 int bicadmm_comm_destroy(bicadmm_comm* comm);
+
+/* ---- in-process emulated communicator (validation of the multi-rank path on one GPU) ----
+ * G "ranks" as G handles of ONE process on one device, each driven by its own host thread
+ * and its own stream: bicadmm_emu_group_create(G), then bicadmm_comm_init_emu for every
+ * rank 0..G-1 (all before any bicadmm_setup), then each thread runs bicadmm_setup /
+ * _iterate / _solve / _finalize on its handle concurrently, exactly as G processes would.
+ * Every AllReduce of the method (Algorithm 2's per-sweep block sum; the outer
+ * Collect) becomes a fixed-order device sum over the members' buffers (ascending
+ * rank), ordered across the members' streams by CUDA events; the threads meet at host
+ * barriers.  No kernel waits on another, so the ranks never need to run concurrently on
+ * the device.  The group owns a scratch buffer per rank (cudaMalloc, freed by
+ * bicadmm_emu_group_destroy, which must follow every bicadmm_comm_destroy of the group).
+ * Errors: BICADMM_ERR_INVALID (G outside [1, 64], rank out of range or registered twice). */
+typedef struct bicadmm_emu_group bicadmm_emu_group;
+int bicadmm_emu_group_create(int world, bicadmm_emu_group** out);
+int bicadmm_comm_init_emu(bicadmm_emu_group* group, int rank, int device, int group_color, bicadmm_comm** out);
+int bicadmm_emu_group_destroy(bicadmm_emu_group* group);
 
 /* Bytes of device workspace needed for this problem on this rank. */
 int bicadmm_workspace_size(const bicadmm_problem* problem, const bicadmm_params* params, size_t* bytes);

@@ -697,6 +697,13 @@ int orc_run(const orc_problem* pb, const orc_params* pr, const int32_t* schedule
             if (res->x) memcpy(res->x + (int64_t)i * len, nodes[i].x, sizeof(double) * (size_t)len);
             if (res->u) memcpy(res->u + (int64_t)i * len, nodes[i].u, sizeof(double) * (size_t)len);
         }
+        if (res->nu) {
+            int64_t off = 0;
+            for (int i = 0; i < N; ++i) {
+                memcpy(res->nu + off, nodes[i].nu, sizeof(double) * (size_t)(nodes[i].m * C));
+                off += nodes[i].m * C;
+            }
+        }
         *res->iters = k;
         *res->converged = converged;
     }

@@ -62,6 +62,7 @@ typedef struct {
     int32_t* iters;       /* [1] */
     int32_t* converged;   /* [1] */
     double* timings;      /* [4]: setup_s, inner_s, outer_s, total_s (wall) or NULL */
+    double* nu;           /* [sum_i m_i*C] final inner duals nu_i (Eq. (23)), nodes concatenated, or NULL */
 } orc_result;
 
 #define ORC_TRACE_COLS 6  /* p_r, d_r, b_r, t, v, tau */

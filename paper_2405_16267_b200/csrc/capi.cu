@@ -14,7 +14,6 @@
 //      a11 (13)      : s
 //      a12 (14)      : v;  (9) u_i += x_i - z;  (15) p_r, d_r, b_r -> host (one sync)
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -26,55 +25,11 @@
 
 #include "../../include/bicadmm.h"
 #include "../../include/bicadmm_ops.h"
+#include "comm.h"
 #include "common.cuh"
 #include "kernels.h"
 
-#if __has_include(<nccl.h>)
-#include <nccl.h>
-#define BIC_HAVE_NCCL 1
-#else
-#define BIC_HAVE_NCCL 0
-#endif
-
 using namespace bic;
-
-// ======================================================================= NCCL (dlopen)
-namespace {
-#if BIC_HAVE_NCCL
-struct NcclApi {
-    void* h = nullptr;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
-    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
-    bool load() {
-        if (h) return true;
-        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) return false;
-        GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
-        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
-        CommSplit = (decltype(CommSplit))dlsym(h, "ncclCommSplit");
-        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
-        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
-        CommCount = (decltype(CommCount))dlsym(h, "ncclCommCount");
-        return GetUniqueId && CommInitRank && CommSplit && AllReduce && CommDestroy && CommCount;
-    }
-};
-NcclApi g_nccl;
-#endif
-}  // namespace
-
-struct bicadmm_comm {
-    int world = 1, rank = 0, device = 0, color = 0, group_size = 1;
-    // BICADMM_NCCL_SELF=1 with world == 1: a real one-rank NCCL communicator, so the
-    // multi-rank code path (collectives, split block sums, eager launches) runs on one GPU
-    bool self = false;
-#if BIC_HAVE_NCCL
-    ncclComm_t world_comm = nullptr, group_comm = nullptr;
-#endif
-};
 
 // ======================================================================= handle
 namespace {
@@ -95,8 +50,7 @@ struct LBlock {      // a local block (i, j), sorted by (node, block)
     bool hpack = false;     // H stored as packed lower tiles (k_symv.cu); C == 1 only
     double* hpart = nullptr;
     double *x, *u, *r, *p, *partial, *pobj;
-    double* fpart;   // fused sweep: [node chunks][nj] partial products of A^T q
-    double* partial2 = nullptr;   // fused v2: [CTAs touching the node][nj]
+    double* partial2 = nullptr;   // single-pass sweep: [clusters touching the node x row groups][nj]
     double* xt = nullptr;         // C > 1: class-major scratch (nj * C)
 };
 struct LNode {
@@ -106,7 +60,6 @@ struct LNode {
     double *nu, *delta, *S, *p_base, *pobj_base, *sq_partial, *obj_partial, *obar;
     int np;
     int64_t nprox_ctas;
-    int64_t ch_rows = 0, nchunks = 0, slot0 = 0, nslots = 0;   // fused sweep chunking
 };
 
 struct Bump {  // 256-byte aligned bump allocator over the workspace (base may be null to size)
@@ -156,6 +109,9 @@ struct bicadmm_handle {
     std::vector<int64_t> m, col_start;
     bicadmm_params prm{};
     bicadmm_comm* comm = nullptr;
+    int gsize = 1;              // ranks of this rank's node group (comm_group_size at setup)
+    double* S_all = nullptr;    // block sums S_i of all local nodes, contiguous (nod[].S point into it)
+    int64_t S_total = 0;
     bool split_blocks = false;  // some node's blocks live on other ranks
     bool any_fat = false;       // some local block takes the Woodbury path
     cudaStream_t st = nullptr;
@@ -183,26 +139,13 @@ struct bicadmm_handle {
     double *x_old = nullptr, *dpart = nullptr, *node_dx = nullptr, *node_res = nullptr;
     double *mask = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_Ap = nullptr, *cg_rhs = nullptr, *cg_sc = nullptr;
     int refit_iters = 0;
-    // fused single-pass sweep (k_fused.cu)
+    // single-pass sweep (k_fused4.cu): CTA-pair clusters over static row ranges
     bool fused = false;
-    FusedTables tb{};
-    FusedNode* fnodes = nullptr;
-    FusedChunk* fchunks = nullptr;
-    FusedSeg* fsegs = nullptr;
-    int* fdone = nullptr;
-    unsigned long long* fcounter = nullptr;
-    int* factive = nullptr;
-    double* fslots = nullptr;
-    int64_t fnch = 0, fslots_n = 0;
-    int fgrid = 0;
+    int fused_kind = 0;            // 0 two-pass, 4 single pass (k_fused4); BICADMM_FIELD_SWEEP_KIND
     std::vector<GemvTDesc> gtf;
-    std::vector<int> active_last;
-    // fused v2 (k_fused2.cu): one CTA per SM, register/smem resident rows
-    int fused_kind = 0;            // 0 two-pass, 1 chunked (k_fused.cu), 2 per-SM rows (k_fused2.cu)
     Fused2Args f2{};
     int f2grid = 0;
-    std::vector<int64_t> f2_cta_lo, f2_cta_n;
-    double* f2slots = nullptr;
+    std::vector<int64_t> f2_cta_lo, f2_cta_n;   // per local node: first cluster touching it, count
     OuterScalars* sc = nullptr;
     int64_t* support = nullptr;
     int64_t* support_count = nullptr;
@@ -230,6 +173,8 @@ struct bicadmm_handle {
     // iteration, terminated on the device; trace rows appended on the device
     double* dtrace = nullptr;         // [kLoopRows][6]
     int* dcount = nullptr;
+    int* label_bad = nullptr;         // setup's label-domain check (BICADMM_ERR_DOMAIN)
+    double* place_chk = nullptr;      // setup's collective placement check: 2 (N M) + 1 doubles
     struct Loop {
         cudaGraphExec_t exec = nullptr;
         int sweeps = -1;
@@ -412,11 +357,18 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     h->x_old = b.arr<double>(lenp * nl);
     h->node_dx = b.arr<double>(P->N);
     h->node_res = b.arr<double>(P->N);
-    // per node
+    // per node; the block sums S_i of all local nodes are contiguous, so Algorithm 2's
+    // per-sweep AllReduce is one collective over all of them
+    int64_t s_total = 0;
+    for (auto& nd : h->nod) s_total += nd.m * C;
+    h->S_all = b.arr<double>(s_total);
+    h->S_total = s_total;
+    int64_t s_off = 0;
     for (auto& nd : h->nod) {
         nd.nu = b.arr<double>(nd.m * C);
         nd.delta = b.arr<double>(nd.m * C);
-        nd.S = b.arr<double>(nd.m * C);
+        nd.S = h->S_all + (base ? s_off : 0);
+        s_off += nd.m * C;
         nd.obar = b.arr<double>(nd.m * C);
         nd.p_base = b.arr<double>(nd.m * C * nd.np);
         nd.pobj_base = b.arr<double>(nd.m * C * nd.np);
@@ -452,6 +404,8 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     h->mask = b.arr<double>(len);
     h->dtrace = b.arr<double>((int64_t)kLoopRows * 6);
     h->dcount = b.arr<int>(2);
+    h->label_bad = b.arr<int>(1);
+    h->place_chk = b.arr<double>(2 * (int64_t)P->N * P->M + 1);
     if (((P->loss == BICADMM_LOGISTIC && C == 1) || P->loss == BICADMM_SOFTMAX) && h->prm.refit) {
         int64_t rows = 0;
         for (auto& nd : h->nod) rows += nd.m;
@@ -496,54 +450,17 @@ static size_t plan(bicadmm_handle* h, const bicadmm_problem* P, void* base) {
     h->cg_Ap = b.arr<double>(len);
     h->cg_rhs = b.arr<double>(len);
     h->cg_sc = b.arr<double>(8);
-    // fused-sweep tables and partials (chunks of ~BICADMM_FUSED_CHUNK_MB MB of A rows per node)
-    {
-        double chunk_mb = 16.0;
-        if (const char* e = getenv("BICADMM_FUSED_CHUNK_MB")) chunk_mb = atof(e) > 0 ? atof(e) : chunk_mb;
-        int64_t nch = 0, slots = 0;
-        const int rpt = fused_rows_per_task();
-        for (auto& nd : h->nod) {
-            int64_t rowb = 0;
-            for (auto& L : h->blk) if (L.li == nd.li) rowb += L.nj * (int64_t)es;
-            int64_t ch = (int64_t)(chunk_mb * 1e6 / (double)std::max<int64_t>(rowb, 1)) / rpt * rpt;
-            nd.ch_rows = std::max<int64_t>(rpt, ch);
-            nd.nchunks = (nd.m + nd.ch_rows - 1) / nd.ch_rows;
-            nd.slot0 = slots;
-            nd.nslots = 0;
-            for (int64_t k = 0; k < nd.nchunks; ++k) {
-                const int64_t rows = std::min(nd.m, (k + 1) * nd.ch_rows) - k * nd.ch_rows;
-                nd.nslots += (rows + rpt - 1) / rpt;
-            }
-            slots += nd.nslots;
-            nch += nd.nchunks;
-        }
-        h->fnch = nch;
-        h->fslots_n = slots;
-        h->fnodes = b.arr<FusedNode>(nl);
-        h->fchunks = b.arr<FusedChunk>(nch);
-        h->fsegs = b.arr<FusedSeg>(2 * nch);
-        h->fdone = b.arr<int>(nch);
-        h->fcounter = b.arr<unsigned long long>(1);
-        h->factive = b.arr<int>(nl);
-        h->fslots = b.arr<double>(slots * rpt);
-        for (auto& L : h->blk) L.fpart = b.arr<double>(h->nod[L.li].nchunks * L.nj * C);
-    }
-    {   // fused v2: static row ranges of one CTA per SM; partials per node over the CTAs touching it
-        // (v4: per CTA pair and row group -- sized for the larger of the two)
+    {   // single-pass sweep: static row ranges of the CTA pairs; partials per node over the
+        // (cluster, row group) pairs touching it
         std::vector<int64_t> rows;
         for (auto& nd : h->nod) rows.push_back(nd.m);
-        touching_units(rows, h->sm_count, h->f2_cta_lo, h->f2_cta_n);
         std::vector<int64_t> lo4, n4;
         touching_units(rows, std::max(1, h->sm_count / 2), lo4, n4);
         int64_t maxc = 0;
         for (auto& L : h->blk) maxc = std::max(maxc, L.nj);
         const int64_t g4 = fused4_groups(P->dtype, maxc);
-        int64_t slots = 0;
-        for (auto& nd : h->nod) slots += h->f2_cta_n[nd.li];
-        h->f2slots = b.arr<double>(slots);
         for (auto& L : h->blk)
-            if (L.jl == 0)
-                L.partial2 = b.arr<double>(std::max<int64_t>({1, h->f2_cta_n[L.li], n4[L.li] * g4}) * L.nj * C);
+            if (L.jl == 0) L.partial2 = b.arr<double>(std::max<int64_t>(1, n4[L.li] * g4) * L.nj * C);
     }
     {   // setup scratch for up to 8 blocks factored in lockstep (BICADMM_FACTOR_BATCH caps it;
         // the extra scratch is limited to ~8 GB)
@@ -588,104 +505,35 @@ static void build_descs(bicadmm_handle* h) {
     }
 }
 
-// Build the fused-sweep task tables (host) and upload them once (setup time).
-static int build_fused(bicadmm_handle* h) {
-    const int nl = (int)h->nod.size();
-    const int rpt = fused_rows_per_task();
-    const int W = fused_strip_width(h->dtype);
-    std::vector<FusedNode> fn(nl);
-    std::vector<FusedChunk> fc;
-    std::vector<FusedSeg> fs;
-    std::vector<int64_t> nA, nB;
-    for (auto& nd : h->nod) {
-        FusedNode& f = fn[nd.li];
-        f = FusedNode{};
-        for (auto& L : h->blk) {
-            if (L.li != nd.li) continue;
-            const int j = L.jl;
-            f.A[j] = L.A; f.lda[j] = L.lda; f.nj[j] = L.nj; f.nstrips[j] = (L.nj + W - 1) / W;
-            f.x[j] = L.x; f.p[j] = L.p; f.partial[j] = L.fpart;
-        }
-        f.nb = nd.np; f.b = nd.b; f.nu = nd.nu; f.delta = nd.delta; f.m = nd.m;
-        int64_t strips = 0;
-        for (int j = 0; j < f.nb; ++j) strips += f.nstrips[j];
-        int64_t slot = nd.slot0;
-        for (int64_t k = 0; k < nd.nchunks; ++k) {
-            FusedChunk c{};
-            c.node = nd.li; c.r0 = k * nd.ch_rows; c.r1 = std::min(nd.m, (k + 1) * nd.ch_rows);
-            c.chunk_in_node = k; c.a_slot0 = slot;
-            const int64_t a = (c.r1 - c.r0 + rpt - 1) / rpt;
-            slot += a;
-            fc.push_back(c);
-            nA.push_back(a);
-            nB.push_back(strips);
-        }
-    }
-    int64_t t = 0;
-    const int64_t nch = (int64_t)fc.size();
-    for (int64_t c = 0; c < nch; ++c) {
-        fs.push_back(FusedSeg{t, 0, (int32_t)c});
-        t += nA[c];
-        if (c >= 1) { fs.push_back(FusedSeg{t, 1, (int32_t)(c - 1)}); t += nB[c - 1]; }
-    }
-    if (nch > 0) { fs.push_back(FusedSeg{t, 1, (int32_t)(nch - 1)}); t += nB[nch - 1]; }
-    H_CUDA(h, cudaMemcpy(h->fnodes, fn.data(), sizeof(FusedNode) * nl, cudaMemcpyHostToDevice));
-    H_CUDA(h, cudaMemcpy(h->fchunks, fc.data(), sizeof(FusedChunk) * nch, cudaMemcpyHostToDevice));
-    H_CUDA(h, cudaMemcpy(h->fsegs, fs.data(), sizeof(FusedSeg) * fs.size(), cudaMemcpyHostToDevice));
-    for (auto& L : h->blk)
-        H_CUDA(h, cudaMemsetAsync(L.fpart, 0, sizeof(double) * h->nod[L.li].nchunks * L.nj * h->C, h->st));
-    H_CUDA(h, cudaMemsetAsync(h->factive, 0xff, sizeof(int) * nl, h->st));
-    h->active_last.assign(nl, 1);
-    h->tb.nodes = h->fnodes; h->tb.chunks = h->fchunks; h->tb.segs = h->fsegs;
-    h->tb.nseg = (int)fs.size(); h->tb.nchunks = (int)nch; h->tb.ntasks = t;
-    h->tb.task_counter = h->fcounter; h->tb.done = h->fdone; h->tb.active = h->factive; h->tb.sq_slots = nullptr;
-    h->fgrid = fused_grid(h->dtype, h->sm_count);
-    h->gtf.clear();
-    for (auto& L : h->blk) {
-        GemvTDesc g{};
-        g.A = L.A; g.lda = L.lda; g.rows = L.m; g.cols = L.nj;
-        g.z = h->z + L.c0 * h->C; g.u = L.u; g.r = L.r; g.partial = L.fpart;
-        g.nchunks = (int32_t)h->nod[L.li].nchunks; g.nstrips = 1; g.chunk_rows = h->nod[L.li].ch_rows;
-        h->gtf.push_back(g);
-    }
-    return BICADMM_OK;
-}
-
-static bool fused2_eligible(bicadmm_handle* h, int kind = 2) {
-    if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes) return false;
+// Single-pass sweep (k_fused4.cu) eligibility: every node's blocks local and one block per
+// node, C == 1, tall blocks, 16-byte row pieces, rows up to fused4_max_cols.
+static bool fused4_eligible(bicadmm_handle* h) {
+    if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes || h->sm_count < 2) return false;
     for (auto& nd : h->nod) if (nd.np != 1) return false;
-    const int64_t cap = kind == 4 ? fused4_max_cols(h->dtype) : kind == 3 ? fused3_max_cols(h->dtype)
-                                                                            : fused2_max_cols(h->dtype);
     const int64_t es = h->dtype == BICADMM_F64 ? 8 : 4;
     for (auto& L : h->blk)
-        if (L.fat || L.nj > cap || (kind == 4 && (L.nj < 8 || (L.nj * es) % 16 || (L.lda * es) % 16))) return false;
-    if (kind == 4 && h->sm_count < 2) return false;
+        if (L.fat || L.nj > fused4_max_cols(h->dtype) || L.nj < 8 || (L.nj * es) % 16 || (L.lda * es) % 16) return false;
     return true;
 }
 
-static int build_fused2(bicadmm_handle* h) {
+static int build_fused4(bicadmm_handle* h) {
     Fused2Args& a = h->f2;
     a = Fused2Args{};
-    int64_t R = 0, maxc = 0, slot = 0;
-    int64_t groups = 1;
-    if (h->fused_kind == 4) {
-        // row ranges per CTA pair (cluster of 2): recompute the touching ranges with G/2 units;
-        // each cluster writes one partial row per row group
-        std::vector<int64_t> rows;
-        for (auto& nd : h->nod) rows.push_back(nd.m);
-        touching_units(rows, h->sm_count / 2, h->f2_cta_lo, h->f2_cta_n);
-        int64_t mc = 0;
-        for (auto& L : h->blk) mc = std::max(mc, L.nj);
-        groups = fused4_groups(h->dtype, mc);
-    }
+    int64_t R = 0, maxc = 0;
+    // row ranges per CTA pair (cluster of 2); each cluster writes one partial row per row group
+    std::vector<int64_t> rows;
+    for (auto& nd : h->nod) rows.push_back(nd.m);
+    touching_units(rows, h->sm_count / 2, h->f2_cta_lo, h->f2_cta_n);
+    int64_t mc = 0;
+    for (auto& L : h->blk) mc = std::max(mc, L.nj);
+    const int64_t groups = fused4_groups(h->dtype, mc);
     a.nn = (int)h->nod.size();
     for (auto& L : h->blk) {
         const LNode& nd = h->nod[L.li];
         const int k = L.li;
         a.A[k] = L.A; a.b[k] = nd.b; a.x[k] = L.x; a.p[k] = L.p; a.nu[k] = nd.nu; a.delta[k] = nd.delta;
         a.partial[k] = L.partial2; a.lda[k] = L.lda; a.ncols[k] = L.nj; a.row_off[k] = R;
-        a.cta_lo[k] = h->f2_cta_lo[k]; a.slot0[k] = slot;
-        slot += h->f2_cta_n[k];
+        a.cta_lo[k] = h->f2_cta_lo[k];
         R += L.m;
         maxc = std::max(maxc, L.nj);
         H_CUDA(h, cudaMemsetAsync(L.partial2, 0, sizeof(double) * std::max<int64_t>(1, h->f2_cta_n[k] * groups) * L.nj,
@@ -693,8 +541,7 @@ static int build_fused2(bicadmm_handle* h) {
     }
     a.total_rows = R;
     a.max_cols_pad = rup(maxc, 4);
-    a.sq_slots = nullptr;
-    h->f2grid = h->fused_kind == 4 ? (h->sm_count / 2) * 2 : h->sm_count;
+    h->f2grid = (h->sm_count / 2) * 2;
     h->gtf.clear();
     for (auto& L : h->blk) {
         GemvTDesc g{};
@@ -728,70 +575,6 @@ const char* bicadmm_rc_string(int rc) {
 
 int64_t bicadmm_launch_count(void) { return g_launches.load(); }
 
-int bicadmm_uid_size(void) {
-#if BIC_HAVE_NCCL
-    return (int)sizeof(ncclUniqueId);
-#else
-    return 128;
-#endif
-}
-
-int bicadmm_get_unique_id(void* uid_out) {
-#if BIC_HAVE_NCCL
-    if (!uid_out) return BICADMM_ERR_INVALID;
-    if (!g_nccl.load()) return BICADMM_ERR_NCCL;
-    ncclUniqueId id;
-    if (g_nccl.GetUniqueId(&id) != ncclSuccess) return BICADMM_ERR_NCCL;
-    memcpy(uid_out, &id, sizeof(id));
-    return BICADMM_OK;
-#else
-    (void)uid_out;
-    return BICADMM_ERR_NCCL;
-#endif
-}
-
-int bicadmm_comm_init(int world, int rank, int device, const void* uid, int group_color, bicadmm_comm** out) {
-    if (!out || world < 1 || rank < 0 || rank >= world || group_color < 0) return BICADMM_ERR_INVALID;
-    bicadmm_comm* c = new bicadmm_comm();
-    c->world = world; c->rank = rank; c->device = device; c->color = group_color;
-    if (cudaSetDevice(device) != cudaSuccess) { delete c; return BICADMM_ERR_CUDA; }
-    const char* se = getenv("BICADMM_NCCL_SELF");
-    c->self = world == 1 && se && atoi(se) != 0;
-    if (world > 1 || c->self) {
-#if BIC_HAVE_NCCL
-        if ((!uid && !c->self) || !g_nccl.load()) { delete c; return BICADMM_ERR_NCCL; }
-        ncclUniqueId id;
-        if (c->self) {
-            if (g_nccl.GetUniqueId(&id) != ncclSuccess) { delete c; return BICADMM_ERR_NCCL; }
-        } else {
-            memcpy(&id, uid, sizeof(id));
-        }
-        if (g_nccl.CommInitRank(&c->world_comm, world, id, rank) != ncclSuccess) { delete c; return BICADMM_ERR_NCCL; }
-        if (g_nccl.CommSplit(c->world_comm, group_color, rank, &c->group_comm, nullptr) != ncclSuccess) {
-            g_nccl.CommDestroy(c->world_comm);
-            delete c;
-            return BICADMM_ERR_NCCL;
-        }
-        g_nccl.CommCount(c->group_comm, &c->group_size);
-#else
-        delete c;
-        return BICADMM_ERR_NCCL;
-#endif
-    }
-    *out = c;
-    return BICADMM_OK;
-}
-
-int bicadmm_comm_destroy(bicadmm_comm* c) {
-    if (!c) return BICADMM_OK;
-#if BIC_HAVE_NCCL
-    if (c->group_comm) g_nccl.CommDestroy(c->group_comm);
-    if (c->world_comm) g_nccl.CommDestroy(c->world_comm);
-#endif
-    delete c;
-    return BICADMM_OK;
-}
-
 int bicadmm_workspace_size(const bicadmm_problem* P, const bicadmm_params* R, size_t* bytes) {
     std::string why;
     if (!bytes) return BICADMM_ERR_INVALID;
@@ -813,18 +596,45 @@ int bicadmm_workspace_size(const bicadmm_problem* P, const bicadmm_params* R, si
 // the handle runs the multi-rank path (NCCL collectives, no graphs)
 static bool multi_rank(const bicadmm_handle* h) { return h->comm && (h->comm->world > 1 || h->comm->self); }
 
+// In-place sum over the node group (group = true: Algorithm 2's per-sweep AllReduce)
+// or over all ranks (the outer "Collect"); a no-op on a single rank.
 static int allreduce(bicadmm_handle* h, double* buf, int64_t count, bool group) {
-#if BIC_HAVE_NCCL
     if (!multi_rank(h) || count <= 0) return BICADMM_OK;
-    ncclComm_t c = group ? h->comm->group_comm : h->comm->world_comm;
-    if (group && h->comm->group_size == 1 && !h->comm->self) return BICADMM_OK;
-    if (g_nccl.AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, c, h->st) != ncclSuccess)
-        return fail(h, BICADMM_ERR_NCCL, "ncclAllReduce");
-    return BICADMM_OK;
-#else
-    (void)buf; (void)count; (void)group;
-    return multi_rank(h) ? fail(h, BICADMM_ERR_NCCL, "built without NCCL") : BICADMM_OK;
-#endif
+    if (group && h->gsize == 1 && !h->comm->self) return BICADMM_OK;
+    std::string why;
+    const int rc = comm_allreduce(h->comm, buf, count, group, h->st, &why);
+    return rc ? fail(h, rc, why) : BICADMM_OK;
+}
+static int allreduce_many(bicadmm_handle* h, double* const* bufs, const int64_t* counts, int n, bool group) {
+    if (!multi_rank(h) || n <= 0) return BICADMM_OK;
+    if (group && h->gsize == 1 && !h->comm->self) return BICADMM_OK;
+    std::string why;
+    const int rc = comm_allreduce_many(h->comm, bufs, counts, n, group, h->st, &why);
+    return rc ? fail(h, rc, why) : BICADMM_OK;
+}
+
+// Collective placement check (multi-rank setup; every rank of the world calls it): each
+// (node, block) pair is held by exactly one rank, and the ranks of a node group together
+// hold every block of each of their nodes -- otherwise the per-sweep AllReduce would sum
+// the wrong blocks or NCCL would wait forever.  All ranks return the same code.
+static int check_placement(bicadmm_handle* h) {
+    const int64_t nm = (int64_t)h->N * h->M;
+    std::vector<double> mask(2 * nm + 1, 0.0);
+    for (auto& L : h->blk) mask[(size_t)L.node * h->M + L.block] = mask[(size_t)(nm + L.node * h->M + L.block)] = 1.0;
+    H_CUDA(h, cudaMemcpyAsync(h->place_chk, mask.data(), sizeof(double) * 2 * nm, cudaMemcpyHostToDevice, h->st));
+    H_RC(h, allreduce(h, h->place_chk, nm, false));        // over all ranks
+    H_RC(h, allreduce(h, h->place_chk + nm, nm, true));    // over this rank's node group
+    H_CUDA(h, cudaMemcpyAsync(mask.data(), h->place_chk, sizeof(double) * 2 * nm, cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    double bad = 0.0;
+    for (int64_t k = 0; k < nm; ++k) bad += mask[(size_t)k] != 1.0;
+    for (auto& nd : h->nod)
+        for (int j = 0; j < h->M; ++j) bad += mask[(size_t)(nm + (int64_t)nd.node * h->M + j)] != 1.0;
+    H_CUDA(h, cudaMemcpyAsync(h->place_chk + 2 * nm, &bad, sizeof(double), cudaMemcpyHostToDevice, h->st));
+    H_RC(h, allreduce(h, h->place_chk + 2 * nm, 1, false));
+    H_CUDA(h, cudaMemcpyAsync(&bad, h->place_chk + 2 * nm, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    H_CUDA(h, cudaStreamSynchronize(h->st));
+    return bad > 0.0 ? BICADMM_ERR_PLACEMENT : BICADMM_OK;
 }
 
 // ======================================================================= setup
@@ -853,32 +663,31 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     if (((uintptr_t)ws) % 256) { delete h; return BICADMM_ERR_INVALID; }
     plan(h, P, ws);
     h->ws_bytes = ws_bytes;
+    h->gsize = comm_group_size(comm);
     if (comm && comm->self) {
         // one-rank NCCL test mode; BICADMM_NCCL_SELF=2 also routes every node's block sum
         // through the per-sweep group AllReduce (the split-block path of block-major placements)
         for (auto& nd : h->nod) if (nd.np != P->M) { delete h; return BICADMM_ERR_PLACEMENT; }
-        h->split_blocks = atoi(getenv("BICADMM_NCCL_SELF")) >= 2;
+        h->split_blocks = comm->self_mode >= 2;
     } else if (comm && comm->world > 1) {
         // a node whose M blocks are not all local has its block sum all-reduced per sweep
         for (auto& nd : h->nod) if (nd.np != P->M) h->split_blocks = true;
-        if (h->split_blocks && comm->group_size * 1 < 2) { delete h; return BICADMM_ERR_PLACEMENT; }
+        if (h->split_blocks && h->gsize < 2) { delete h; return BICADMM_ERR_PLACEMENT; }
     } else {
         for (auto& nd : h->nod) if (nd.np != P->M) { delete h; return BICADMM_ERR_PLACEMENT; }
         if ((int)h->nod.size() != P->N) { delete h; return BICADMM_ERR_PLACEMENT; }
     }
+    if (multi_rank(h) && !comm->self) {
+        const int rc2 = check_placement(h);
+        if (rc2) { delete h; return rc2; }
+    }
     build_descs(h);
     {   // inner-sweep schedule (bicadmm_params.sweep)
-        bool ok1 = !h->split_blocks && h->C == 1 && (int)h->nod.size() <= kMaxDesc;
-        for (auto& L : h->blk) ok1 = ok1 && !L.fat;
-        for (auto& nd : h->nod) ok1 = ok1 && nd.np <= kFMaxBlk;
-        const bool ok2 = fused2_eligible(h);
-        const bool ok3 = fused2_eligible(h, 3);
-        const bool ok4 = fused2_eligible(h, 4);
-        const char* fk = getenv("BICADMM_FUSED_KIND");   // tuning: force 1 (chunked) or 2 (per-SM rows)
+        const bool ok4 = fused4_eligible(h);
         int kind = 0;
         if (R->sweep == 2) {
-            if (!ok1 && !ok2 && !ok3 && !ok4) { delete h; return BICADMM_ERR_INVALID; }
-            kind = ok4 ? 4 : ok3 ? 3 : ok2 ? 2 : 1;
+            if (!ok4) { delete h; return BICADMM_ERR_INVALID; }
+            kind = 4;
         } else if (R->sweep == 0) {
             // auto: the CTA-pair single-pass sweep (k_fused4) where eligible -- measured on B200
             // (profiles/r01_summary.md) 1.45 ms vs 2.43 ms for the two HBM passes on configs[1];
@@ -891,19 +700,10 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             const int64_t row_bytes = maxc * (P->dtype == BICADMM_F64 ? 8 : 4);
             kind = ok4 && row_bytes >= 14336 ? 4 : 0;
         }
-        if (fk && kind != 0) {
-            const int want = atoi(fk);
-            if (want == 1 && ok1) kind = 1;
-            if (want == 2 && ok2) kind = 2;
-            if (want == 3 && ok3) kind = 3;
-            if (want == 4 && ok4) kind = 4;
-        }
         h->fused_kind = kind;
         h->fused = kind != 0;
-        if (kind == 1 && build_fused(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
-        if (kind >= 2 && build_fused2(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
+        if (kind == 4 && build_fused4(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
     }
-    // labels are device memory; their domain check (ERR_DOMAIN) is done by the binding
     if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
         cudaMallocHost(&h->host_i64, sizeof(int64_t) * 4) != cudaSuccess) {
         bicadmm_destroy(h);
@@ -932,6 +732,10 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             return BICADMM_ERR_CUDA;
         }
     }
+    // label domain (BICADMM_ERR_DOMAIN): one pass over every local node's labels; the flag
+    // is read back with setup's final synchronisation
+    // (launched per node right after its first block's ready event, below)
+    if (zero(h->label_bad, sizeof(int))) { bicadmm_destroy(h); return BICADMM_ERR_CUDA; }
     // one-time block factors (a0)
     cudaEventRecord(h->e0, h->st);
     const double c = R->lambda / (double)P->N + R->rho_c;   // 1/(N gamma) + rho_c
@@ -943,6 +747,10 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             const int64_t ldg = rup(L.kd, 8);
             double* G = h->gram + k * h->gram_stride;
             if (L.ready && cudaStreamWaitEvent(h->st, (cudaEvent_t)L.ready, 0) != cudaSuccess) {
+                rc = BICADMM_ERR_CUDA;
+                break;
+            }
+            if (L.jl == 0 && launch_check_labels(P->dtype, P->loss, P->C, L.m, h->nod[L.li].b, h->label_bad, h->st)) {
                 rc = BICADMM_ERR_CUDA;
                 break;
             }
@@ -972,7 +780,12 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
     }
     for (auto& L : h->blk) L.ready = nullptr;   // not retained (bicadmm_block.ready_event)
     cudaEventRecord(h->e1, h->st);
-    if (cudaEventSynchronize(h->e1) != cudaSuccess) { bicadmm_destroy(h); return BICADMM_ERR_CUDA; }
+    if (cudaMemcpyAsync(h->host_i32, h->label_bad, sizeof(int), cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
+        cudaStreamSynchronize(h->st) != cudaSuccess) {
+        bicadmm_destroy(h);
+        return BICADMM_ERR_CUDA;
+    }
+    if (h->host_i32[0]) { bicadmm_destroy(h); return BICADMM_ERR_DOMAIN; }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->e0, h->e1);
     h->ms_setup = ms;
@@ -1033,27 +846,13 @@ static int inner_sweep_fused(bicadmm_handle* h, const std::vector<int>& active_n
                                   cudaMemcpyDeviceToDevice, h->st));
     H_RC(h, hx.launch(h));
     mark(2);
-    for (size_t li = 0; li < h->nod.size() && h->fused_kind == 1; ++li)
-        if (h->active_last[li] != (int)act[li]) {
-            H_CUDA(h, cudaMemsetAsync(h->factive + li, act[li] ? 0xff : 0, sizeof(int), h->st));
-            h->active_last[li] = act[li];
-        }
-    if (h->fused_kind == 1) {
-        FusedTables tb = h->tb;
-        tb.sq_slots = tol ? h->fslots : nullptr;
-        H_RC(h, launch_fused_sweep(h->dtype, tb, h->loss, h->M, h->prm.rho_l, h->fgrid, h->st));
-    } else {
+    {
         Fused2Args a = h->f2;
-        a.sq_slots = tol ? h->f2slots : nullptr;
         for (size_t li = 0; li < h->nod.size(); ++li) {
             a.active[li] = act[li];
             a.e2row[li] = tol ? h->nod[li].S : nullptr;   // S is unused on the single-rank fused path
         }
-        static const bool fast_dbg = getenv("BICADMM_FUSED_DEBUG_LSPROX") != nullptr;   // timing experiments only
-        const int floss = fast_dbg ? BICADMM_LS : h->loss;
-        if (h->fused_kind == 4) H_RC(h, launch_fused4(h->dtype, a, floss, h->prm.rho_l, h->f2grid, h->st));
-        else if (h->fused_kind == 3) H_RC(h, launch_fused3(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
-        else H_RC(h, launch_fused2(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
+        H_RC(h, launch_fused4(h->dtype, a, h->loss, h->prm.rho_l, h->f2grid, h->st));
     }
     mark(3);
     if (h->prof) {
@@ -1125,8 +924,16 @@ static int inner_sweep(bicadmm_handle* h, const std::vector<int>& active_nodes, 
     mark(4);
     if (h->split_blocks) {
         H_RC(h, launch_psum(h->C, px.data(), (int)px.size(), nullptr, h->st));
-        // all local nodes' S are contiguous only per node: one AllReduce per node (batched by NCCL group)
-        for (int li : active_nodes) H_RC(h, allreduce(h, h->nod[li].S, h->nod[li].m * h->C, true));
+        // Algorithm 2's AllReduce: every local node's S_i in one collective (they are
+        // contiguous); with a subset of nodes active (tolerance mode) one grouped call
+        if (active_nodes.size() == h->nod.size()) {
+            H_RC(h, allreduce(h, h->S_all, h->S_total, true));
+        } else {
+            std::vector<double*> bufs;
+            std::vector<int64_t> cnts;
+            for (int li : active_nodes) { bufs.push_back(h->nod[li].S); cnts.push_back(h->nod[li].m * h->C); }
+            H_RC(h, allreduce_many(h, bufs.data(), cnts.data(), (int)bufs.size(), true));
+        }
     }
     mark(5);
     H_RC(h, launch_prox(h->loss, h->dtype, h->C, h->M, h->prm.rho_l, px.data(), (int)px.size(), h->st));
@@ -1245,19 +1052,11 @@ static int inner_criteria(bicadmm_handle* h, const std::vector<int>& active, std
     std::vector<int64_t> cnt;
     std::vector<int32_t> node;
     for (int li : active) {
-        if (h->fused_kind == 2) {
-            ptr.push_back(h->f2slots + h->f2.slot0[li]);
-            cnt.push_back(h->f2_cta_n[li]);
-        } else if (h->fused_kind == 1) {
-            ptr.push_back(h->fslots + h->nod[li].slot0 * fused_rows_per_task());
-            cnt.push_back(h->nod[li].nslots * fused_rows_per_task());
-        } else {
-            ptr.push_back(h->nod[li].sq_partial);
-            cnt.push_back(h->nod[li].nprox_ctas);
-        }
+        ptr.push_back(h->nod[li].sq_partial);
+        cnt.push_back(h->nod[li].nprox_ctas);
         node.push_back(h->nod[li].node);
     }
-    if (h->fused_kind >= 3) {
+    if (h->fused) {   // the single-pass kernel leaves (abar - omega)^2 per row in S
         for (int li : active) H_RC(h, launch_sum(h->nod[li].m, h->nod[li].S, h->node_res + h->nod[li].node, h->st));
     } else {
         H_RC(h, launch_seg_sums(ptr.data(), cnt.data(), node.data(), (int)ptr.size(), h->node_res, h->st));
@@ -1477,8 +1276,8 @@ static int refit_apply(bicadmm_handle* h, const double* v, double* out, bool rhs
             ProxNode p{};
             p.p = nd.pobj_base; p.np = nd.np; p.pstride = nd.m; p.m = nd.m; p.S = nd.S;
             H_RC(h, launch_psum(1, &p, 1, nullptr, h->st));
-            if (h->split_blocks) H_RC(h, allreduce(h, nd.S, nd.m, true));
         }
+        if (h->split_blocks) H_RC(h, allreduce(h, h->S_all, h->S_total, true));   // C == 1 here
     } else {
         for (auto& nd : h->nod) H_RC(h, launch_to_f64(h->dtype, nd.m, nd.b, nd.S, h->st));
     }
@@ -1683,10 +1482,10 @@ static int do_finalize(bicadmm_handle* h) {
         if (h->split_blocks) {
             p.S = nd.S;
             H_RC(h, launch_psum(h->C, &p, 1, nullptr, h->st));
-            H_RC(h, allreduce(h, nd.S, nd.m * h->C, true));
         }
         px.push_back(p);
     }
+    if (h->split_blocks) H_RC(h, allreduce(h, h->S_all, h->S_total, true));
     H_RC(h, launch_loss(h->loss, h->dtype, h->C, px.data(), (int)px.size(), h->st));
     H_CUDA(h, cudaMemsetAsync(h->node_obj, 0, sizeof(double) * h->N, h->st));
     for (auto& nd : h->nod) {
@@ -1704,7 +1503,7 @@ static int do_finalize(bicadmm_handle* h) {
     H_CUDA(h, cudaMemcpyAsync(nobj.data() + h->N, h->wsum, sizeof(double), cudaMemcpyDeviceToHost, h->st));
     H_CUDA(h, cudaStreamSynchronize(h->st));
     double obj = 0.0;
-    const double gs = (multi_rank(h) && h->split_blocks) ? (double)h->comm->group_size : 1.0;
+    const double gs = (multi_rank(h) && h->split_blocks) ? (double)h->gsize : 1.0;
     for (int i = 0; i < h->N; ++i) obj += nobj[i] / gs;
     obj += 0.5 * h->prm.lambda * nobj[h->N];
     h->objective = obj;

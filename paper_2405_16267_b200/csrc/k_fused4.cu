@@ -36,7 +36,12 @@ constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp 
 constexpr int kF4MainT = 32 * kF4Main;         // 384
 constexpr int kF4RingMax = 32;                 // half-row ring depth (runtime nring <= 32 = kF4Q, by smem)
 constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
-constexpr int kF4Q = 32;                       // dot / q slots (>= delay + lag window)
+// dot / q / token slots, indexed by row mod kF4Q.  A slot is reused kF4Q rows later; the
+// peer CTA may run ahead of this CTA's prox warps by at most nring + ngrp (D + 1) rows (its
+// producer is held by its ring, its main warps by the q of rows that need this CTA's dots),
+// so f4_launch keeps nring + ngrp (D + 1) <= kF4Q (with 32 slots, n = 2000 FP64,
+// 26 ring slots and 6 row groups exceeded it)
+constexpr int kF4Q = 64;
 
 // The logistic prox sits on every row's critical path, so its FP64
 // pieces are latency-trimmed (tools/prox_latency2.cu: 2,220 -> 1,250 cycles per prox,
@@ -555,8 +560,10 @@ static int f4_delay(int nring, int ngrp) {
 
 template <typename T, int GR>
 static int f4_launch(int E, int ngrp, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
-    const int nring = f4_ring(a, sizeof(T));
+    int nring = f4_ring(a, sizeof(T));
     if (nring < 4 || ngrp >= nring - 1) return BICADMM_ERR_INVALID;
+    while (nring > 4 && nring + ngrp * (f4_delay(nring, ngrp) + 1) > kF4Q) --nring;   // slot reuse bound
+    if (nring + ngrp * (f4_delay(nring, ngrp) + 1) > kF4Q) return BICADMM_ERR_INVALID;
     const size_t smem = (size_t)nring * f4_slot_bytes(a, sizeof(T));
 #define F4_CASE(EE)                                                                                            \
     case EE: {                                                                                                 \

@@ -38,12 +38,9 @@
 
 namespace bic {
 
-constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 32;   // tile M (columns i), N (columns j), K (rows per stage)
+constexpr int kOzBM = 128, kOzBK = 32;               // tile M (columns i), K (rows per stage)
 constexpr int kOzSMax = 7;                            // digits S; weights 2 .. S + 1
-constexpr int kOzStages = 5;
 constexpr int kOzRoundStages = 16384 / kOzBK;         // stages per int32 accumulation round
-constexpr int kOzThreads = 192;                       // 4 epilogue warps, 1 MMA warp, 1 TMA warp
-constexpr size_t kOzStageBytes = (size_t)kOzSMax * (kOzBM + kOzBN) * kOzBK;   // 42 KB
 constexpr int kOzRowChunk = 32768;                    // rows of A split per launch pair
 
 __device__ __forceinline__ uint32_t oz_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -168,8 +165,7 @@ __global__ void __launch_bounds__(128) k_oz_split_rows(const T* __restrict__ src
 
 // ----------------------------------------------------------------------------- GEMM
 // Operands by bulk copy (pre-swizzled SWIZZLE_32B: one K = 32-byte row per column,
-// 8-column atoms of 256 B), 4-stage ring, one tcgen05.mma (M 128, N 64, K 32) per slice
-// pair per stage.
+// 8-column atoms of 256 B), 4-stage ring, tcgen05.mma (M 128, N 128, K 32) per slice pair.
 __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -206,22 +202,6 @@ __device__ __forceinline__ void oz_bulk(void* dst, const void* src, uint32_t byt
 __device__ __forceinline__ void oz_mbar_arrive(uint64_t* b) {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(oz_smem(b)) : "memory");
 }
-__device__ __forceinline__ void oz_ld64(uint32_t taddr, uint32_t (&v)[64]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,"
-        "%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
-          "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]),
-          "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]),
-          "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
-          "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
-        : "r"(taddr));
-}
-
 struct OzArgs {
     int64_t M, N;            // true sizes of C (rows i: A-operand rows; columns j: B-operand rows)
     int64_t Mp, Np, Kp;      // padded A / B operand rows, padded summed index of this chunk
@@ -237,168 +217,9 @@ struct OzArgs {
     int64_t ldc;
 };
 
-// One 128 x 64 tile of C = alpha A B^T-ish (both operands K-major digit slices) + beta C + diag I
-__global__ void __launch_bounds__(kOzThreads, 1)
-    k_oz_mm(const __grid_constant__ OzArgs a) {
-    extern __shared__ __align__(1024) uint8_t oz_sm_raw[];
-    uint8_t* oz_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_sm_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[kOzStages], empty[kOzStages], acc_full, acc_empty;
-    __shared__ uint32_t tmem_base;
-    int64_t bi, bj;
-    if (a.lower) {   // column block bi of 128 (rows of C), bj of 64 with 64 bj < 128 (bi + 1)
-        int64_t t = blockIdx.x;
-        bi = 0;
-        while (t >= 2 * bi + 2) { t -= 2 * bi + 2; ++bi; }
-        bj = t;
-    } else {
-        bi = (int64_t)blockIdx.x / a.ntj;
-        bj = (int64_t)blockIdx.x % a.ntj;
-    }
-    const int64_t i0 = bi * kOzBM, j0 = bj * kOzBN;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // summed range of this tile (structural zeros skipped), relative to the chunk, in stages
-    int64_t klo = 0, khi = a.K;
-    if (a.k_lo == 1) klo = i0;
-    if (a.k_lo == 2) klo = j0;
-    if (a.k_lo == 3) klo = i0 > j0 ? i0 : j0;
-    if (a.k_hi == 1 && i0 + kOzBM < khi) khi = i0 + kOzBM;
-    if (a.k_hi == 2 && j0 + kOzBN < khi) khi = j0 + kOzBN;
-    klo = (klo > a.r_begin ? klo : a.r_begin) - a.r_begin;
-    khi = (khi < a.r_begin + a.Kp ? khi : a.r_begin + a.Kp) - a.r_begin;
-    const int st0 = (int)(klo / kOzBK);
-    const int st1 = khi > klo ? (int)((khi + kOzBK - 1) / kOzBK) : st0;
-    const int nstage = st1 - st0;
-    const uint32_t bytes_stage = (uint32_t)(kOzSMax * (kOzBM + kOzBN) * kOzBK);
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(oz_smem(&tmem_base)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (tid == 0) {
-        for (int s = 0; s < kOzStages; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&full[s])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&empty[s])));
-        }
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(oz_smem(&acc_full)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(oz_smem(&acc_empty)), "r"(128));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_base;
-    const int nround = (nstage + kOzRoundStages - 1) / kOzRoundStages;
-
-    if (warp == 5) {
-        // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            for (int q = 0; q < nstage; ++q) {
-                const int sb = q % kOzStages;
-                if (q >= kOzStages) oz_mbar_wait(&empty[sb], (uint32_t)((q / kOzStages - 1) & 1));
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(oz_smem(&full[sb])),
-                             "r"(bytes_stage) : "memory");
-                uint8_t* base = oz_sm + (size_t)sb * kOzStageBytes;
-                const int64_t kc = st0 + q, KC = a.Kp / kOzBK;
-#pragma unroll
-                for (int s = 0; s < kOzSMax; ++s) {
-                    const int64_t ra = (s * KC + kc) * a.Mp + i0, rbb = (s * KC + kc) * a.Np + j0;
-                    oz_bulk(base + (size_t)s * kOzBM * kOzBK, a.da + ra * kOzBK, kOzBM * kOzBK, &full[sb]);
-                    oz_bulk(base + (size_t)kOzSMax * kOzBM * kOzBK + (size_t)s * kOzBN * kOzBK, a.db + rbb * kOzBK,
-                            kOzBN * kOzBK, &full[sb]);
-                }
-            }
-        }
-    } else if (warp == 4) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            // idesc: S32 accumulate, s8 x s8, K-major A and B, N = 64, M = 128
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kOzBN >> 3) << 17) |
-                                   ((uint32_t)(kOzBM >> 4) << 24);
-            const uint32_t smem0 = oz_smem(oz_sm);
-            int q = 0;
-            for (int rd = 0; rd < nround; ++rd) {
-                if (rd > 0) oz_mbar_wait(&acc_empty, (uint32_t)((rd - 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const int q_end = (rd + 1) * kOzRoundStages < nstage ? (rd + 1) * kOzRoundStages : nstage;
-                const int q_begin = q;
-                for (; q < q_end; ++q) {
-                    const int sb = q % kOzStages;
-                    oz_mbar_wait(&full[sb], (uint32_t)((q / kOzStages) & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    // descriptors: the start-address field is bits [0,14) in 16-byte units, so the
-                    // slice tiles of this stage are fixed offsets from the stage's base descriptor
-                    const uint64_t dA0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes));
-                    const uint64_t dB0 = oz_desc(smem0 + (uint32_t)(sb * kOzStageBytes) + (uint32_t)(kOzSMax * kOzBM * kOzBK));
-                    const uint32_t first = q == q_begin ? 1u : 0u;
-#pragma unroll
-                    for (int sa = 1; sa <= kOzSMax; ++sa)
-#pragma unroll
-                        for (int sbk = 1; sbk <= kOzSMax; ++sbk) {
-                            if (sa + sbk > kOzSMax + 1) continue;
-                            const int w = sa + sbk;
-                            const uint32_t dt = tmem + (uint32_t)((w - 2) * kOzBN);
-                            const uint64_t da = dA0 + (uint64_t)(((sa - 1) * kOzBM * kOzBK) >> 4);
-                            const uint64_t db = dB0 + (uint64_t)(((sbk - 1) * kOzBN * kOzBK) >> 4);
-                            // the first product of each weight in a round overwrites its accumulator
-                            const uint32_t accum = (sa == 1) ? (first ^ 1u) : 1u;
-                            asm volatile(
-                                "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(dt),
-                                "l"(da), "l"(db), "r"(idesc), "r"(accum));
-                        }
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                        oz_smem(&empty[sb])));
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    oz_smem(&acc_full)));
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ epilogue (warps 0-3)
-        double acc[kOzBN];
-#pragma unroll
-        for (int c = 0; c < kOzBN; ++c) acc[c] = 0.0;
-        for (int rd = 0; rd < nround; ++rd) {
-            oz_mbar_wait_sleep(&acc_full, (uint32_t)(rd & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t lane_addr = tmem + ((uint32_t)(32 * warp) << 16);
-            for (int w = 2; w <= kOzSMax + 1; ++w) {   // fixed order w = 2 .. S + 1
-                uint32_t v[64];
-                oz_ld64(lane_addr + (uint32_t)((w - 2) * kOzBN), v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const double sc = ldexp(1.0, -7 * w);
-#pragma unroll
-                for (int c = 0; c < kOzBN; ++c) acc[c] = fma((double)(int32_t)v[c], sc, acc[c]);
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            oz_mbar_arrive(&acc_empty);
-        }
-        // C[i][j] = alpha 2^(e_i + f_j) acc + beta C[i][j] (+ diag on i == j)
-        const int64_t i = i0 + 32 * warp + lane;
-        if (i < a.M) {
-            const int ei = oz_exp(__longlong_as_double((long long)a.amax[i]));
-            double* crow = a.C + i * a.ldc;
-#pragma unroll
-            for (int c = 0; c < kOzBN; ++c) {
-                const int64_t j = j0 + c;
-                if (j >= a.N || (a.lower && j > i)) continue;
-                const int ej = oz_exp(__longlong_as_double((long long)a.bmax[j]));
-                double v = a.alpha * ldexp(acc[c], ei + ej);
-                if (a.beta != 0.0) v += a.beta * crow[j];
-                if (i == j) v += a.diag;
-                crow[j] = v;
-                if (a.mirror && j < i) a.C[j * a.ldc + i] = v;
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-}
-
 // ----------------------------------------------------------------------------- N = 128, two passes
-// At N = 64 a tcgen05.mma kind::i8 costs ~48 cycles instead of 32 (tools/tc_i8_rate.cu);
-// N = 128 runs at the full rate (64 cycles for twice the work).  Seven 128 x 128 int32
+// (An earlier N = 64 single-pass variant was slower: at N = 64 a tcgen05.mma kind::i8 costs
+// ~48 cycles instead of 32, tools/tc_i8_rate.cu; N = 128 runs at the full rate.)  Seven 128 x 128 int32
 // accumulators do not fit the 512 TMEM columns, so each tile streams its summed range
 // twice: pass 0 the weights 2..5 (digits 1..4, 10 products, 4 accumulators = 512
 // columns), pass 1 the weights 6..8 (all digits, 18 products, 3 accumulators).  The FP64
@@ -589,11 +410,6 @@ __global__ void __launch_bounds__(kOz2Threads, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-static bool oz_n128() {
-    static const bool on = [] { const char* e = getenv("BICADMM_OZ_N64"); return !(e && atoi(e) != 0); }();
-    return on;
-}
-
 // ----------------------------------------------------------------------------- host
 static int64_t oz_rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -655,11 +471,8 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
     unsigned long long* amax = reinterpret_cast<unsigned long long*>(base + off);
     unsigned long long* bmax = g.same ? amax : amax + Mp;
     static bool attr = false;
-    const bool n128 = oz_n128();
-    const size_t smem = (n128 ? kOz2Stages * kOz2StageBytes : kOzStages * kOzStageBytes) + 1024;   // + alignment slack
+    const size_t smem = kOz2Stages * kOz2StageBytes + 1024;   // + alignment slack
     if (!attr) {
-        BIC_CUDA(cudaFuncSetAttribute(k_oz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kOzStages * kOzStageBytes + 1024)));
         BIC_CUDA(cudaFuncSetAttribute(k_oz_mm128, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kOz2Stages * kOz2StageBytes + 1024)));
         attr = true;
@@ -677,9 +490,9 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
         }
     }
     const int64_t ntb = Mp / kOzBM;
-    const int64_t bn = n128 ? kOz2BN : kOzBN, ntj = oz_rup(g.N, bn) / bn;
-    // lower: sum over bi of (bi + 1) 128-wide or (2 bi + 2) 64-wide column tiles
-    const int64_t tiles = g.lower ? (n128 ? ntb * (ntb + 1) / 2 : ntb * (ntb + 1)) : ntb * ntj;
+    const int64_t ntj = oz_rup(g.N, kOz2BN) / kOz2BN;
+    // lower: sum over bi of (bi + 1) 128-wide column tiles
+    const int64_t tiles = g.lower ? ntb * (ntb + 1) / 2 : ntb * ntj;
     for (int64_t r_begin = 0; r_begin < (g.K > 0 ? g.K : 1); r_begin += kOzRowChunk) {
         const int64_t rows = g.K - r_begin < kOzRowChunk ? g.K - r_begin : kOzRowChunk;
         const int64_t Kp = oz_rup(rows > 0 ? rows : 1, kOzBK);
@@ -699,8 +512,7 @@ int launch_gemm_tc(const OzGemm& g, void* scratch, size_t scratch_bytes, cudaStr
         oa.K = g.K; oa.r_begin = r_begin; oa.amax = amax; oa.bmax = bmax; oa.da = da; oa.db = db;
         oa.alpha = g.alpha; oa.beta = r_begin > 0 ? 1.0 : g.beta; oa.diag = r_begin > 0 ? 0.0 : g.diag;
         oa.C = g.C; oa.ldc = g.ldc;
-        if (n128) k_oz_mm128<<<(unsigned)tiles, kOz2Threads, smem, s>>>(oa);
-        else k_oz_mm<<<(unsigned)tiles, kOzThreads, smem, s>>>(oa);
+        k_oz_mm128<<<(unsigned)tiles, kOz2Threads, smem, s>>>(oa);
         BIC_LAUNCHED();
     }
     return BICADMM_OK;

@@ -6,6 +6,8 @@
 // SPD and, for kappa << m with unit-norm columns, condition ~1, so CG reaches
 // 1e-15 relative residual in a few tens of iterations.  Dot products are
 // single-CTA fixed-order reductions (bit-identical on every rank).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -95,6 +97,32 @@ __global__ void k_to_f64(int64_t n, const T* __restrict__ src, double* __restric
 int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s) {
     if (dtype == BICADMM_F64) k_to_f64<double><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, (const double*)src, dst);
     else k_to_f64<float><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, (const float*)src, dst);
+    BIC_LAUNCHED();
+    return BICADMM_OK;
+}
+
+// Label domain of the loss (bicadmm.h BICADMM_ERR_DOMAIN, DESIGN R12): logistic and
+// hinge labels in {-1, +1}, softmax class ids integral in [0, C), LS labels finite.  Any
+// violation sets *bad = 1 (pre-zeroed; read back once by bicadmm_setup).
+template <typename T>
+__global__ void k_check_labels(int64_t n, const T* __restrict__ b, int loss, int C, int* bad) {
+    int my = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const double v = (double)b[r];
+        bool ok;
+        if (loss == BICADMM_LOGISTIC || loss == BICADMM_HINGE) ok = v == 1.0 || v == -1.0;
+        else if (loss == BICADMM_SOFTMAX) ok = v >= 0.0 && v < (double)C && v == floor(v);
+        else ok = isfinite(v);
+        my |= ok ? 0 : 1;
+    }
+    if (__syncthreads_or(my) && threadIdx.x == 0) *bad = 1;
+}
+
+int launch_check_labels(int dtype, int loss, int C, int64_t n, const void* b, int* bad, cudaStream_t s) {
+    if (n <= 0) return BICADMM_OK;
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 1024);
+    if (dtype == BICADMM_F64) k_check_labels<double><<<g, 256, 0, s>>>(n, (const double*)b, loss, C, bad);
+    else k_check_labels<float><<<g, 256, 0, s>>>(n, (const float*)b, loss, C, bad);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }

@@ -170,38 +170,7 @@ int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, dou
 int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s);
 constexpr int kUThreads = 256;
 
-// ---------------------------------------------------------------- fused single-pass sweep (k_fused.cu)
-constexpr int kFMaxBlk = 16;   // local blocks per node in the fused kernel
-struct FusedNode {
-    const void* A[kFMaxBlk];
-    int64_t lda[kFMaxBlk], nj[kFMaxBlk], nstrips[kFMaxBlk];
-    const double* x[kFMaxBlk];
-    double* p[kFMaxBlk];
-    double* partial[kFMaxBlk];   // [nchunks of the node][nj]
-    int nb;
-    const void* b;
-    double *nu, *delta;
-    int64_t m;
-};
-struct FusedChunk { int32_t node; int64_t r0, r1, chunk_in_node, a_slot0; };
-struct FusedSeg { int64_t t0; int32_t type, chunk; };   // type 0 = phase A rows, 1 = phase B strips
-struct FusedTables {
-    const FusedNode* nodes;
-    const FusedChunk* chunks;
-    const FusedSeg* segs;
-    int nseg, nchunks;
-    int64_t ntasks;
-    unsigned long long* task_counter;
-    int* done;
-    const int* active;      // per local node
-    double* sq_slots;       // optional: per A task x 8 rows, (abar - omega)^2 (tol mode)
-};
-int launch_fused_sweep(int dtype, const FusedTables& tb, int loss, int M, double rho, int grid, cudaStream_t s);
-int fused_grid(int dtype, int sm_count);
-int fused_strip_width(int dtype);
-int fused_rows_per_task();
-
-// ---------------------------------------------------------------- fused sweep v2 (k_fused2.cu)
+// ---------------------------------------------------------------- single-pass sweep (k_fused4.cu)
 constexpr int kF2MaxNodes = 32;
 struct Fused2Args {
     const void* A[kF2MaxNodes];
@@ -210,21 +179,16 @@ struct Fused2Args {
     double* p[kF2MaxNodes];
     double* nu[kF2MaxNodes];
     double* delta[kF2MaxNodes];
-    double* partial[kF2MaxNodes];     // [cta - cta_lo][ncols]
-    int64_t lda[kF2MaxNodes], ncols[kF2MaxNodes], row_off[kF2MaxNodes], cta_lo[kF2MaxNodes], slot0[kF2MaxNodes];
+    double* partial[kF2MaxNodes];     // [(cluster - cta_lo) x row groups][ncols]
+    int64_t lda[kF2MaxNodes], ncols[kF2MaxNodes], row_off[kF2MaxNodes], cta_lo[kF2MaxNodes];
     int32_t active[kF2MaxNodes];      // inactive nodes (tol mode / schedule) keep all their state
-    double* e2row[kF2MaxNodes];       // fused v3, tol mode: per-row (abar - omega)^2 (else null)
+    double* e2row[kF2MaxNodes];       // tol mode: per-row (abar - omega)^2 (else null)
     int nn;
     int64_t total_rows, max_cols_pad;
-    double* sq_slots;                 // optional per-(node, cta) sum of (abar - omega)^2 (tol mode)
 };
-int launch_fused2(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
-int fused2_max_cols(int dtype);
-int launch_fused3(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
 int fused4_max_cols(int dtype);
 int fused4_groups(int dtype, int64_t max_cols);   // row groups of the CTA-pair sweep (partials per group)
-int fused3_max_cols(int dtype);
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)
 int launch_dot(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
@@ -233,6 +197,8 @@ int launch_ridge_mask(int64_t n, const double* mask, const double* v, double lam
 int launch_cg_xr(int64_t n, const double* sc, const double* p, const double* Ap, double* x, double* r, cudaStream_t s);
 int launch_cg_p(int64_t n, const double* sc, const double* r, double* p, cudaStream_t s);
 int launch_to_f64(int dtype, int64_t n, const void* src, double* dst, cudaStream_t s);
+// *bad = 1 if a label lies outside the loss domain (BICADMM_ERR_DOMAIN); *bad pre-zeroed
+int launch_check_labels(int dtype, int loss, int C, int64_t n, const void* b, int* bad, cudaStream_t s);
 // logistic refit on the support (k_vec.cu; DESIGN R29)
 int launch_rf_gather(int dtype, const void* A, int64_t lda, int64_t m, int64_t c0, int64_t nj, const int64_t* sup,
                      const int64_t* cnt, double* AT, int64_t kp, int64_t row_off, cudaStream_t s, int C = 1);

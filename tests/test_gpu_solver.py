@@ -65,8 +65,8 @@ CASES = [
 def test_fp64_iterates_match_oracle(bc, orc, case, sweep):
     _, N, m, n, kappa, loss, M, K, K_in = case[:9]
     C = case[9] if len(case) > 9 else 1
-    if C > 1 and sweep == 2:
-        pytest.skip("fused single-pass sweep is C == 1 only (softmax runs two-pass)")
+    if sweep == 2 and (C > 1 or M > 1 or n % 2):
+        pytest.skip("the single-pass sweep takes one block per node, C == 1 and 16-byte half-rows")
     solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, sweep=sweep)
     _check_fp64(solver, rep, zs, xs, ref, K)
 
@@ -173,7 +173,7 @@ def test_tol_mode_inner_loop_and_replay(bc, orc, sweep):
     # counts replayed by the oracle reproduce the GPU iterates to 1e-9, and agree
     # with the oracle's own tolerance-mode counts (boundary flips are allowed but rare)
     P = dg.generate(3, 300, 120, 6, "logistic", seed=21)
-    cs = dg.block_partition(120, 2)
+    cs = dg.block_partition(120, 2 if sweep == 1 else 1)   # the single-pass sweep: one block per node
     K = 8
     prm = dict(kappa=6, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=60, refit=0,
                eps_p=0.0, eps_d=0.0, eps_b=0.0)
@@ -188,34 +188,14 @@ def test_tol_mode_inner_loop_and_replay(bc, orc, sweep):
     assert np.mean(counts == own["inner_counts"]) >= 0.8
 
 
-def test_fused_chunking_many_chunks(bc, orc, monkeypatch=None):
-    # the fused sweep over many small chunks (forces many A/B tasks and cross-chunk waits)
-    import os
-    os.environ["BICADMM_FUSED_CHUNK_MB"] = "0.05"
-    try:
-        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 2100, 333, 9, "logistic", 2, 6, 4, sweep=2)
-    finally:
-        del os.environ["BICADMM_FUSED_CHUNK_MB"]
-    for k in range(6):
-        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9
-
-
-@pytest.mark.parametrize("kind", ["1", "2", "3", "4"])
-def test_fused_kinds_single_block(bc, orc, kind):
-    # both fused implementations on single-block nodes (k_fused.cu chunked / k_fused2.cu per-SM rows),
-    # including ragged n (odd column count) and FP32 storage
-    import os
-    os.environ["BICADMM_FUSED_KIND"] = kind
-    try:
-        for dtype, tol in ((torch.float64, 1e-9), (torch.float32, 1e-4)):
-            n = 304 if kind == "4" else 301     # the CTA-pair kernel needs n % 8 == 0
-            solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 777, n, 9, "logistic", 1, 6, 5, sweep=2, dtype=dtype)
-            assert solver.sweep_kind()[0] == int(kind)
-            for k in range(6):
-                assert _rel(zs[k], ref["z_trace"][k]) <= tol, (kind, dtype, k)
-            assert solver.support().tolist() == ref["support"].tolist()
-    finally:
-        del os.environ["BICADMM_FUSED_KIND"]
+def test_fused_single_block_fp64_fp32(bc, orc):
+    # the single-pass CTA-pair sweep (k_fused4) on single-block nodes, FP64 and FP32 storage
+    for dtype, tol in ((torch.float64, 1e-9), (torch.float32, 1e-4)):
+        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 777, 304, 9, "logistic", 1, 6, 5, sweep=2, dtype=dtype)
+        assert solver.sweep_kind()[0] == 4
+        for k in range(6):
+            assert _rel(zs[k], ref["z_trace"][k]) <= tol, (dtype, k)
+        assert solver.support().tolist() == ref["support"].tolist()
 
 
 # Woodbury fat-block path (DESIGN R27): blocks with m_i < n_j factor the m_i x m_i
@@ -363,7 +343,6 @@ def test_fused4_row_groups(bc, orc, groups):
     # several nodes so that node boundaries fall inside clusters
     import os
     os.environ["BICADMM_F4_GROUPS"] = groups
-    os.environ["BICADMM_FUSED_KIND"] = "4"
     try:
         solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 5, 611, 496, 9, "logistic", 1, 6, 5, sweep=2)
         assert solver.sweep_kind() == (4, 0)
@@ -372,21 +351,15 @@ def test_fused4_row_groups(bc, orc, groups):
         assert solver.support().tolist() == ref["support"].tolist()
     finally:
         del os.environ["BICADMM_F4_GROUPS"]
-        del os.environ["BICADMM_FUSED_KIND"]
 
 
 def test_fused4_ragged_width(bc, orc):
     # n_j = 306 (FP64: 2448-byte rows, not a multiple of 64 bytes) on the CTA-pair kernel
-    import os
-    os.environ["BICADMM_FUSED_KIND"] = "4"
-    try:
-        solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 700, 306, 9, "logistic", 1, 6, 5, sweep=2)
-        assert solver.sweep_kind() == (4, 0)
-        for k in range(6):
-            assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, k
-        assert solver.support().tolist() == ref["support"].tolist()
-    finally:
-        del os.environ["BICADMM_FUSED_KIND"]
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, 3, 700, 306, 9, "logistic", 1, 6, 5, sweep=2)
+    assert solver.sweep_kind() == (4, 0)
+    for k in range(6):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, k
+    assert solver.support().tolist() == ref["support"].tolist()
 
 
 @pytest.mark.parametrize("loss", ["ls", "hinge"])
@@ -547,3 +520,37 @@ def test_nccl_one_rank_path_matches_local(bc, case, split):
         assert abs(a["obj"] - b["obj"]) <= 1e-11 * abs(a["obj"])
     assert np.array_equal(a["sup"], b["sup"])
     assert _rel(b["xf"], a["xf"]) <= 1e-11
+
+
+@pytest.mark.parametrize("loss,C,bad", [("logistic", 1, 0.5), ("hinge", 1, 0.0), ("softmax", 3, 3.0),
+                                        ("softmax", 3, 1.5), ("softmax", 3, -1.0), ("ls", 1, float("nan"))])
+def test_domain_error_from_the_c_abi(bc, loss, C, bad):
+    # BICADMM_ERR_DOMAIN (bicadmm.h) comes from bicadmm_setup itself (a device pass over
+    # the labels), not from the Python wrapper: raw ctypes structs, no BiCADMM class
+    import ctypes as ct
+    P = dg.generate(2, 64, 32, 3, loss, seed=5, C=C)
+    A = [a.cuda().contiguous() for a in P.A]
+    b = [x.cuda().contiguous() for x in P.b]
+    for fail_node in (None, 1):
+        if fail_node is not None:
+            b[fail_node][17] = bad
+        cs = np.array([0, 32], dtype=np.int64)
+        m = np.array([64, 64], dtype=np.int64)
+        blocks = (bc.bicadmm_block * 2)(*[bc.bicadmm_block(i, 0, A[i].data_ptr(), 32, None) for i in range(2)])
+        bptr = (ct.c_void_p * 2)(*[x.data_ptr() for x in b])
+        prob = bc.bicadmm_problem(2, 1, C, bc.LOSSES[loss], bc.F64, 2, 32, m.ctypes.data_as(ct.POINTER(ct.c_int64)),
+                                  cs.ctypes.data_as(ct.POINTER(ct.c_int64)), blocks, bptr)
+        prm = bc.Params(kappa=3).struct()
+        nbytes = ct.c_size_t(0)
+        assert bc.lib().bicadmm_workspace_size(ct.byref(prob), ct.byref(prm), ct.byref(nbytes)) == 0
+        ws = torch.empty(nbytes.value + 256, dtype=torch.uint8, device="cuda")
+        base = ws.data_ptr() + (-ws.data_ptr()) % 256
+        h = ct.c_void_p()
+        rc = bc.lib().bicadmm_setup(ct.byref(prob), ct.byref(prm), None, ct.c_void_p(base), nbytes.value,
+                                    ct.c_void_p(torch.cuda.current_stream().cuda_stream), ct.byref(h))
+        if fail_node is None:
+            assert rc == bc.OK
+            bc.lib().bicadmm_destroy(h)
+        else:
+            assert rc == bc.ERR_DOMAIN
+            assert not h.value

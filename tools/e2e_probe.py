@@ -46,7 +46,7 @@ def run(mode):
             t_.record_stream(st)
     t1 = time.time()
     blocks = [(k, 0, dA[k], evs[k]) if evs[k] is not None else (k, 0, dA[k]) for k in range(N)]
-    s = bc.BiCADMM(None, db, "logistic", prm, cs, blocks=blocks, check_domain=False)
+    s = bc.BiCADMM(None, db, "logistic", prm, cs, blocks=blocks)
     t2 = time.time()
     E[2].record(st)
     for _ in range(5):
