@@ -1,0 +1,124 @@
+"""Oracle parity at the kernel instantiations the benchmarks run.
+
+The small-shape parity cases in test_gpu_solver.py only reach the narrow template
+instances of the single-pass sweep (elements per lane E <= 4).  Here the GPU path runs
+at the row widths of BASELINE.json's configs -- so the SAME compiled kernels the bench
+times are compared with the FP64 oracle (oracle/orc.c), iterate by iterate:
+
+* n = 10,000 (configs[1], the headline; k_fused4 E = 14, one row group), FP64 and FP32;
+* n = 12,500 (configs[2]'s block width n_j; E = 17, 4-slot ring, axpy delay 1), FP64, FP32;
+* n = 6,250 (configs[4]'s block width; E = 17, two row groups), hinge;
+* n = 4,000 (Table 1 rows; E = 16, three row groups), LS;
+* configs[3]'s block shape: softmax, C = 10, M = 8 blocks of 2,512 columns (n = 20,096,
+  blocks aligned to 16 columns as bench.py places them), the DMMA GEMV-T-C / GEMV-C
+  kernels at their multi-strip widths.
+
+m_i is just above n_j (tall blocks: the Gram/factor path of every config) so that the
+oracle's setup (an m n^2 / 2 Gram and an unblocked Cholesky) stays within minutes.
+Bar (north star; DESIGN R22): FP64 1e-9 relative for z^k, x^k, t, v and the residuals,
+identical support, objective 1e-9; FP32 storage 1e-4 against the same FP64 oracle run.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2405_16267_b200 import datagen as dg  # noqa: E402
+
+_ORACLE_CACHE = {}
+
+
+@pytest.fixture(scope="module")
+def bc():
+    from paper_2405_16267_b200 import build
+    build.build()
+    from paper_2405_16267_b200 import bicadmm
+    bicadmm.lib()
+    return bicadmm
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+# name: (N, m_i, n, M, kappa, loss, C, K_outer, K_in, block align)
+WIDE = {
+    "n10000_configs1": (1, 10_100, 10_000, 1, 20, "logistic", 1, 3, 3, 4),
+    "n12500_configs2_block": (1, 12_600, 12_500, 1, 25, "ls", 1, 3, 2, 4),
+    "n6250_configs4_block": (2, 6_300, 6_250, 1, 15, "hinge", 1, 3, 3, 4),
+    "n4000_table1": (2, 4_100, 4_000, 1, 40, "ls", 1, 4, 4, 4),
+    "softmax_configs3_blocks": (1, 2_600, 20_096, 8, 60, "softmax", 10, 3, 2, 16),
+}
+
+
+def _data(name):
+    N, m, n, M, kappa, loss, C, K, K_in, al = WIDE[name]
+    P = dg.generate(N, m, n, kappa, loss, C=C, seed=101)
+    cs = dg.block_partition(n, M, align=al)
+    return P, cs
+
+
+def _oracle(orc, name):
+    if name not in _ORACLE_CACHE:
+        N, m, n, M, kappa, loss, C, K, K_in, al = WIDE[name]
+        P, cs = _data(name)
+        lid = {"ls": orc.LS, "logistic": orc.LOGISTIC, "hinge": orc.HINGE, "softmax": orc.SOFTMAX}[loss]
+        prm = orc.Params(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+        ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], lid, P.C, np.array(cs)),
+                      prm, trace_z=True, trace_x=True)
+        _ORACLE_CACHE[name] = (P, cs, ref)
+    return _ORACLE_CACHE[name]
+
+
+def _gpu(bc, P, cs, name, dtype):
+    N, m, n, M, kappa, loss, C, K, K_in, al = WIDE[name]
+    prm = bc.Params(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], loss, prm, cs, C=P.C)
+    zs, xs = [], []
+    for _ in range(K):
+        s.iterate(1)
+        zs.append(s.z)
+        xs.append(s.get(bc.FIELD_X_LOCAL))
+    rep = s.finalize()
+    return s, rep, np.array(zs), np.array(xs)
+
+
+def _check(s, rep, zs, xs, ref, K, tol):
+    tr_g, tr_o = s.trace(), ref["trace"]
+    assert tr_g.shape == tr_o.shape
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= tol, (k, _rel(zs[k], ref["z_trace"][k]))
+        assert _rel(xs[k], ref["x_trace"][k].ravel()) <= tol, (k, _rel(xs[k], ref["x_trace"][k].ravel()))
+        t_o, v_o = tr_o[k, 3], tr_o[k, 4]
+        assert abs(tr_g[k, 3] - t_o) <= tol * abs(t_o)
+        assert abs(tr_g[k, 4] - v_o) <= tol * max(abs(v_o), abs(t_o))
+        for c in (0, 1):   # p_r, d_r relative to their first-iteration scale (DESIGN R22)
+            assert abs(tr_g[k, c] - tr_o[k, c]) <= tol * max(abs(tr_o[k, c]), abs(tr_o[0, c])), (k, c)
+        assert abs(tr_g[k, 2] - tr_o[k, 2]) <= tol * max(abs(tr_o[k, 2]), abs(t_o))
+    assert s.support().tolist() == ref["support"].tolist()
+    assert abs(rep.objective - ref["objective"]) <= tol * abs(ref["objective"])
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("name", ["n10000_configs1", "n12500_configs2_block", "n6250_configs4_block",
+                                  "n4000_table1"])
+def test_single_pass_sweep_at_bench_widths(bc, orc, name, dt):
+    if dt == "f32" and name in ("n6250_configs4_block", "n4000_table1"):
+        pytest.skip("FP32 is checked at the two widest instances")
+    P, cs, ref = _oracle(orc, name)
+    dtype = torch.float64 if dt == "f64" else torch.float32
+    s, rep, zs, xs = _gpu(bc, P, cs, name, dtype)
+    assert s.sweep_kind()[0] == 4, s.sweep_kind()   # the auto-chosen CTA-pair single-pass kernel
+    _check(s, rep, zs, xs, ref, WIDE[name][7], 1e-9 if dt == "f64" else 1e-4)
+    s.close()
+
+
+def test_softmax_c10_m8_blocks_at_configs3_width(bc, orc):
+    name = "softmax_configs3_blocks"
+    P, cs, ref = _oracle(orc, name)
+    assert [cs[j + 1] - cs[j] for j in range(8)] == [2512] * 8
+    s, rep, zs, xs = _gpu(bc, P, cs, name, torch.float64)
+    _check(s, rep, zs, xs, ref, WIDE[name][7], 1e-9)
+    s.close()
