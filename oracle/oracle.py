@@ -49,7 +49,8 @@ class _Result(ct.Structure):
     _fields_ = [("z", _pd), ("s", _pd), ("t", _pd), ("v", _pd), ("x", _pd), ("u", _pd),
                 ("trace", _pd), ("inner_counts", _pi32), ("z_trace", _pd), ("x_trace", _pd),
                 ("support", _pi64), ("support_len", _pi64), ("x_final", _pd),
-                ("objective", _pd), ("iters", _pi32), ("converged", _pi32), ("timings", _pd), ("nu", _pd)]
+                ("objective", _pd), ("iters", _pi32), ("converged", _pi32), ("timings", _pd), ("nu", _pd),
+                ("step_s", _pd)]
 
 
 def build(force: bool = False) -> str:
@@ -192,7 +193,7 @@ def run(problem: Problem, params: Params, schedule=None, trace_z: bool = False, 
                support=np.zeros(max(params.kappa, 1), dtype=np.int64),
                support_len=np.zeros(1, dtype=np.int64), x_final=np.zeros(ln),
                objective=np.zeros(1), iters=np.zeros(1, dtype=np.int32),
-               converged=np.zeros(1, dtype=np.int32), timings=np.zeros(4),
+               converged=np.zeros(1, dtype=np.int32), timings=np.zeros(4), step_s=np.zeros(K),
                nu=np.zeros(max(1, int(sum(a.shape[0] for a in problem.A)) * C)))
     zt = np.zeros((K, ln)) if trace_z else None
     xt = np.zeros((K, N, ln)) if trace_x else None
@@ -201,7 +202,7 @@ def run(problem: Problem, params: Params, schedule=None, trace_z: bool = False, 
                   _d(zt) if zt is not None else None, _d(xt) if xt is not None else None,
                   out["support"].ctypes.data_as(_pi64), out["support_len"].ctypes.data_as(_pi64),
                   _d(out["x_final"]), _d(out["objective"]), out["iters"].ctypes.data_as(_pi32),
-                  out["converged"].ctypes.data_as(_pi32), _d(out["timings"]), _d(out["nu"]))
+                  out["converged"].ctypes.data_as(_pi32), _d(out["timings"]), _d(out["nu"]), _d(out["step_s"]))
     sched = None
     if schedule is not None:
         schedule = np.ascontiguousarray(schedule, dtype=np.int32)
@@ -215,6 +216,7 @@ def run(problem: Problem, params: Params, schedule=None, trace_z: bool = False, 
                 support=out["support"][:int(out["support_len"][0])], x_final=out["x_final"],
                 objective=float(out["objective"][0]), iters=it, converged=bool(out["converged"][0]),
                 timings=dict(zip(("setup_s", "inner_s", "outer_s", "total_s"), out["timings"].tolist())),
+                step_s=out["step_s"][:it],
                 nu=np.split(out["nu"][:int(sum(a.shape[0] for a in problem.A)) * C], np.cumsum([a.shape[0] * C for a in problem.A])[:-1]),
                 z_trace=None if zt is None else zt[:it], x_trace=None if xt is None else xt[:it])
 

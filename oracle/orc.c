@@ -655,6 +655,7 @@ int orc_run(const orc_problem* pb, const orc_params* pr, const int32_t* schedule
         if (res->x_trace)
             for (int i = 0; i < N; ++i) memcpy(res->x_trace + ((int64_t)k * N + i) * len, nodes[i].x, sizeof(double) * (size_t)len);
         t_outer += orc_now() - tb;
+        if (res->step_s) res->step_s[k] = orc_now() - ta;
         if (p_r <= pr->eps_p && d_r <= pr->eps_d && b_r <= pr->eps_b) { converged = 1; ++k; break; }
     }
 

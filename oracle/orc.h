@@ -63,6 +63,8 @@ typedef struct {
     int32_t* converged;   /* [1] */
     double* timings;      /* [4]: setup_s, inner_s, outer_s, total_s (wall) or NULL */
     double* nu;           /* [sum_i m_i*C] final inner duals nu_i (Eq. (23)), nodes concatenated, or NULL */
+    double* step_s;       /* [max_outer] wall seconds of each outer iteration (inner + global step) or NULL;
+                             timing only (bench.py's reference arm times exactly K steps after W) */
 } orc_result;
 
 #define ORC_TRACE_COLS 6  /* p_r, d_r, b_r, t, v, tau */

@@ -36,7 +36,18 @@ def test_bench_line_contract_c1():
 
 
 def test_bench_reference_arm_line():
-    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1")
+    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-m", "5000", "--cpu-n", "1000")
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_block_placement_small():
+    # the block-major data path (datagen.generate_blocks, placement.plan) on one GPU:
+    # configs[3]'s softmax with 8 feature blocks at a small size
+    d = _run("--config", "C4", "--m", "4000", "--n", "2048", "--kappa", "40", "--steps", "3", "--warmup", "3",
+             "--no-cpu", "--no-ttt")
+    assert d["config"]["placement"].startswith("block-major") and d["config"]["local_blocks"] == 8
+    assert d["scaling"] == "strong" and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0
+
