@@ -603,6 +603,7 @@ def main():
         world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
         N = args.nodes * world if args.placement == "node" else args.nodes
         me = pl.plan(world, N, args.M, args.placement)[rank]
+        time.sleep(0.3 * rank)   # one line per rank, not interleaved
         print(json.dumps({"dry_run": True, "rank": rank, "world": world, "placement": args.placement,
                           "node_group": me.node_group, "blocks": me.blocks}), flush=True)
         return

@@ -93,7 +93,7 @@ def lib() -> ct.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = os.environ.get("BICADMM_LIB_PATH", LIB_PATH)   # A/B timing of alternative builds only
+    path = os.environ.get("BICADMM_LIB_PATH") or LIB_PATH   # A/B timing of alternative builds only
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with __graft_entry__.build() "
                            "(python -m paper_2405_16267_b200.build); there is no CPU fallback")

@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libbicadmm.so")
-SOURCES = ["k_gemv.cu", "k_gemv_c.cu", "k_gemv_dmma.cu", "k_prox.cu", "k_factor.cu", "k_gram_tc.cu", "k_outer.cu", "k_vec.cu", "k_fused4.cu", "k_symv.cu", "comm.cu", "capi.cu", "ops.cu"]
+SOURCES = ["k_gemv.cu", "k_gemv_c.cu", "k_gemv_dmma.cu", "k_prox.cu", "k_factor.cu", "k_gram_tc.cu", "k_outer.cu", "k_vec.cu", "k_fused4.cu", "k_fused4_r1.cu", "k_fused4_r2.cu", "k_fused4_r4.cu", "k_symv.cu", "comm.cu", "capi.cu", "ops.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
