@@ -56,7 +56,10 @@ constexpr int kGdKC = 64;                     // k per staged chunk
 
 __device__ __forceinline__ int xs_swz(int k, int c) { return k * 16 + (c ^ (4 * ((k >> 2) & 3))); }
 
-template <typename T, int NT>
+// XC = 2: classes 8 and 9 (C = 9 or 10) as two DFMAs per element instead of a second,
+// three-quarters-empty n-tile: DMMA and DFMA share the FP64 datapath (tools/fp64_rate.cu:
+// 37 TFLOP/s DMMA, 33 DFMA, 33 mixed), so this is 10 classes of work instead of 16.
+template <typename T, int NT, int XC = 0>
 __global__ void __launch_bounds__(kGdThreads, 2) k_gemv_dmma(const __grid_constant__ GemvBatchD B, int C) {
     __shared__ double xs[2][kGdKC * 16];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
@@ -72,10 +75,14 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_gemv_dmma(const __grid_consta
         rowp[i] = static_cast<const T*>(D.A) + (r < D.rows ? r : D.rows - 1) * D.lda;
     }
     double acc[kGdR][NT][2];
+    double accx[kGdR][XC > 0 ? XC : 1];   // classes 8.. of row 8i + g over this thread's k
 #pragma unroll
-    for (int i = 0; i < kGdR; ++i)
+    for (int i = 0; i < kGdR; ++i) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[i][nt][0] = acc[i][nt][1] = 0.0;
+#pragma unroll
+        for (int e = 0; e < (XC > 0 ? XC : 1); ++e) accx[i][e] = 0.0;
+    }
     const int64_t cols = D.cols;
     const double* x = D.x;
     // staging: thread e holds elements e, e + 256, e + 512, e + 768 of the 64 x 16 chunk
@@ -124,11 +131,29 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_gemv_dmma(const __grid_consta
                 for (int i = 0; i < kGdR; ++i)
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) dmma(acc[i][nt], a[i][j], b[nt]);
+                if constexpr (XC > 0) {
+                    // X[k][8], X[k][9]: adjacent after the swizzle (8 ^ 4m, 9 ^ 4m)
+                    const double2 xe = *reinterpret_cast<const double2*>(&xs[buf][xs_swz(kl, 8)]);
+#pragma unroll
+                    for (int i = 0; i < kGdR; ++i) {
+                        accx[i][0] = fma(a[i][j], xe.x, accx[i][0]);
+                        if (XC > 1) accx[i][XC > 1 ? 1 : 0] = fma(a[i][j], xe.y, accx[i][XC > 1 ? 1 : 0]);
+                    }
+                }
             }
         }
         if (more) store_chunk(buf ^ 1);
         __syncthreads();
         buf ^= 1;
+    }
+    if constexpr (XC > 0) {   // the 4 lanes t of a row group hold disjoint k: fixed-order butterfly
+#pragma unroll
+        for (int i = 0; i < kGdR; ++i)
+#pragma unroll
+            for (int e = 0; e < XC; ++e) {
+                accx[i][e] += __shfl_xor_sync(0xffffffffu, accx[i][e], 1);
+                accx[i][e] += __shfl_xor_sync(0xffffffffu, accx[i][e], 2);
+            }
     }
 #pragma unroll
     for (int i = 0; i < kGdR; ++i) {
@@ -141,11 +166,22 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_gemv_dmma(const __grid_consta
                 const int c = nt * 8 + 2 * t + e;
                 if (c < C) D.y[r * C + c] = D.alpha * acc[i][nt][e];
             }
+        if constexpr (XC > 0)
+            if (t == 0)
+#pragma unroll
+                for (int e = 0; e < XC; ++e)
+                    if (8 + e < C) D.y[r * C + 8 + e] = D.alpha * accx[i][e];
     }
 }
 
 bool gemv_c_dmma_enabled() {
     static bool on = [] { const char* e = getenv("BICADMM_GEMVC_DMMA"); return !(e && atoi(e) == 0); }();
+    return on;
+}
+
+// 9 <= C <= 10: one n-tile on DMMA plus DFMA for classes 8-9 (BICADMM_GEMVC_MIXED=0: two n-tiles)
+static bool gemv_c_mixed() {
+    static const bool on = [] { const char* e = getenv("BICADMM_GEMVC_MIXED"); return !(e && atoi(e) == 0); }();
     return on;
 }
 
@@ -165,9 +201,11 @@ int launch_gemv_c_dmma(int dtype, int C, GemvDesc* d, int nd, cudaStream_t s) {
         const unsigned blocks = (unsigned)t;
         if (dtype == BICADMM_F64) {
             if (C <= 8) k_gemv_dmma<double, 1><<<blocks, kGdThreads, 0, s>>>(B, C);
+            else if (C <= 10 && gemv_c_mixed()) k_gemv_dmma<double, 1, 2><<<blocks, kGdThreads, 0, s>>>(B, C);
             else k_gemv_dmma<double, 2><<<blocks, kGdThreads, 0, s>>>(B, C);
         } else {
             if (C <= 8) k_gemv_dmma<float, 1><<<blocks, kGdThreads, 0, s>>>(B, C);
+            else if (C <= 10 && gemv_c_mixed()) k_gemv_dmma<float, 1, 2><<<blocks, kGdThreads, 0, s>>>(B, C);
             else k_gemv_dmma<float, 2><<<blocks, kGdThreads, 0, s>>>(B, C);
         }
         BIC_LAUNCHED();
@@ -327,7 +365,7 @@ __device__ __forceinline__ void tt_wait(uint64_t* b, unsigned parity) {
         if (it > (1ll << 26)) asm volatile("trap;");
 }
 
-template <int NT>
+template <int NT, int XC = 0>
 __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_constant__ GemvTBatchD B, int C) {
     extern __shared__ __align__(128) unsigned char tt_sm[];
     double* As = reinterpret_cast<double*>(tt_sm);        // [ST][RS][LD]
@@ -382,10 +420,14 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
     }
     const int g = lane >> 2, t = lane & 3;
     double acc[4][NT][2];
+    double accx[4][XC > 0 ? XC : 1];   // classes 8.. of column cbase + 8j over this thread's rows
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[j][nt][0] = acc[j][nt][1] = 0.0;
+#pragma unroll
+        for (int e = 0; e < (XC > 0 ? XC : 1); ++e) accx[j][e] = 0.0;
+    }
     const int cbase = 32 * (warp & 7) + g;   // this thread's columns cbase + 8j
     const int half = warp >> 3;               // rows [half RS/2, (half + 1) RS/2) of each stage
     for (int st = 0; st < nstage; ++st) {
@@ -415,6 +457,22 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
             for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) dmma(acc[j][nt], a[j], q[nt]);
+            if constexpr (XC > 0) {   // Q[row i][8], Q[row i][9] (C even: 16-byte aligned pair)
+                double2 qe = make_double2(0.0, 0.0);
+                if (ok) {
+                    qe = *reinterpret_cast<const double2*>(ps + i * C + 8);
+                    if (D.delta) {
+                        const double2 de = *reinterpret_cast<const double2*>(ds + i * C + 8);
+                        qe.x += de.x;
+                        qe.y += de.y;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    accx[j][0] = fma(a[j], qe.x, accx[j][0]);
+                    if (XC > 1) accx[j][XC > 1 ? 1 : 0] = fma(a[j], qe.y, accx[j][XC > 1 ? 1 : 0]);
+                }
+            }
         }
         __syncwarp();
         if (lane == 0) asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(
@@ -422,16 +480,29 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
     }
     // fixed-order sum of the two row halves through shared memory (the ring is drained: every
     // stage was consumed by all consumer warps before they reach this barrier)
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTtCW) : "memory");
-    double* red = As + (size_t)(threadIdx.x & 255) * (4 * NT * 2);
-    if (half == 1) {
+    if constexpr (XC > 0) {   // the 4 lanes t hold disjoint rows of the same columns
 #pragma unroll
         for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < XC; ++e) {
+                accx[j][e] += __shfl_xor_sync(0xffffffffu, accx[j][e], 1);
+                accx[j][e] += __shfl_xor_sync(0xffffffffu, accx[j][e], 2);
+            }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTtCW) : "memory");
+    constexpr int kRed = 4 * NT * 2 + 4 * XC;
+    double* red = As + (size_t)(threadIdx.x & 255) * kRed;
+    if (half == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 red[(j * NT + nt) * 2] = acc[j][nt][0];
                 red[(j * NT + nt) * 2 + 1] = acc[j][nt][1];
             }
+#pragma unroll
+            for (int e = 0; e < XC; ++e) red[4 * NT * 2 + j * XC + e] = accx[j][e];
+        }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kTtCW) : "memory");
     if (half == 1) return;
@@ -449,6 +520,11 @@ __global__ void __launch_bounds__(kTtThreads, 1) k_gemv_t_dmma_tma(const __grid_
                 const int k = nt * 8 + 2 * t + e;
                 if (k < C) out[l * C + k] = acc[j][nt][e] + red[(j * NT + nt) * 2 + e];
             }
+        if constexpr (XC > 0)
+            if (t == 0)
+#pragma unroll
+                for (int e = 0; e < XC; ++e)
+                    if (8 + e < C) out[l * C + 8 + e] = accx[j][e] + red[4 * NT * 2 + j * XC + e];
     }
 }
 
@@ -470,6 +546,8 @@ int launch_gemv_t_c_dmma(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s)
         if (!attr) {
             if (cudaFuncSetAttribute(k_gemv_t_dmma_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTtSmem) !=
                     cudaSuccess ||
+                cudaFuncSetAttribute(k_gemv_t_dmma_tma<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTtSmem) !=
+                    cudaSuccess ||
                 cudaFuncSetAttribute(k_gemv_t_dmma_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTtSmem) !=
                     cudaSuccess)
                 return BICADMM_ERR_CUDA;
@@ -487,6 +565,7 @@ int launch_gemv_t_c_dmma(int dtype, int C, GemvTDesc* d, int nd, cudaStream_t s)
             B.total_ctas = t;
             if (t == 0) continue;
             if (C <= 8) k_gemv_t_dmma_tma<1><<<(unsigned)t, kTtThreads, kTtSmem, s>>>(B, C);
+            else if (C <= 10 && gemv_c_mixed()) k_gemv_t_dmma_tma<1, 2><<<(unsigned)t, kTtThreads, kTtSmem, s>>>(B, C);
             else k_gemv_t_dmma_tma<2><<<(unsigned)t, kTtThreads, kTtSmem, s>>>(B, C);
             BIC_LAUNCHED();
         }
