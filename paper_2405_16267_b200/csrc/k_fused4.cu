@@ -99,6 +99,15 @@ extern "C" int bicadmm_debug_f4_trace(void* dev_buf) {   // trace builds only (B
     return r1 ? r1 : r2 ? r2 : r4;
 }
 
+// check builds only (BIC_F4_CHECK): tag mismatches seen so far (0 in product builds)
+extern "C" unsigned long long bicadmm_debug_f4_errors(void) {
+    unsigned long long a = 0, b = 0, c = 0;
+    f4_errors_r1(&a);
+    f4_errors_r2(&b);
+    f4_errors_r4(&c);
+    return a + b + c;
+}
+
 int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s) {
     int64_t maxc = 0;
     for (int k = 0; k < a.nn; ++k) maxc = a.ncols[k] > maxc ? a.ncols[k] : maxc;

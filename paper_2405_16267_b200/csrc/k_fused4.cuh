@@ -49,7 +49,11 @@ constexpr int kF4Main = BIC_F4_MAIN;           // main warps per CTA
 constexpr int kF4Prox = 3;                     // prox warps per CTA
 constexpr int kF4Threads = 32 * (kF4Main + kF4Prox + 1);   // + 1 producer warp = 512
 constexpr int kF4MainT = 32 * kF4Main;         // 384
+#ifdef BIC_F4_CHECK
+constexpr int kF4RingBytes = (kF4Main > 12 ? 202 : 208) * 1024;   // the check build's slot tags take 1.5 KB
+#else
 constexpr int kF4RingBytes = (kF4Main > 12 ? 204 : 210) * 1024;   // dynamic smem of the ring (static smem grows with kF4Main)
+#endif
 constexpr int kF4RingMax = 32;                 // ring depth in batches (runtime nring <= 32, by smem)
 constexpr int kF4D = 2;                        // axpy delay (rows) when the axpy reads the smem ring
 constexpr int kF4PF = 4;                       // prox input lookahead (rows of a prox worker)
@@ -245,6 +249,21 @@ static __device__ long long* g_f4_trace = nullptr;   // one per translation unit
 #endif
 
 
+// Protocol check (variant builds only: tools/build_variant.sh ... -DBIC_F4_CHECK; compute-
+// sanitizer is closed on this GPU pool): every row slot carries the global row index it
+// holds -- written by each CTA's main warps for its own dots, sent to the peer with the dots
+// (one more st.async per row, counted in the peer's expect_tx), and written by the prox warps
+// next to q.  The prox warps check both dot tags of every row they reduce and the main warps
+// the q tag of every row they accumulate; a slot reused too early or a barrier phase that
+// completed for the wrong row shows up as a tag mismatch, counted in g_f4_errors
+// (bicadmm_debug_f4_errors).
+#ifdef BIC_F4_CHECK
+static __device__ unsigned long long g_f4_errors = 0;
+#define F4_CHECK_ON 1
+#else
+#define F4_CHECK_ON 0
+#endif
+
 struct F4Batch {
     int64_t r0;
     int n;
@@ -284,6 +303,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
     __shared__ double dotp[kF4Q][2 * kF4Main];            // [row slot][cta * W + warp of the group]
     __shared__ double qv[kF4Q];
     __shared__ double tok[kF4Q];                          // CTA 1 -> CTA 0: row inputs read
+#if F4_CHECK_ON
+    __shared__ long long ctag[kF4Q], ptag[kF4Q], qtag[kF4Q];   // row index held by a slot (own / peer dots, q)
+    for (int i = threadIdx.x; i < kF4Q; i += blockDim.x) ctag[i] = ptag[i] = qtag[i] = -1;
+#endif
     __shared__ __align__(8) uint64_t bar_full[kF4RingMax], bar_empty[kF4RingMax], bar_dot[QB], bar_q[QB];
     const unsigned h = cluster_rank();                     // column half owned by this CTA
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,8 +497,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                             *dp = dot[k];
                             if (!(BIC_F4_EXP & 8)) st_async_f64(mapa(smem_u32(dp), peer), dot[k], pbar);
                         }
+#if F4_CHECK_ON
+                    if (wig == 0)
+                        for (int k = 0; k < nbd; ++k) {   // own tag, and the row index to the peer's ptag
+                            ctag[qb * R + k] = bd.r0 + k;
+                            st_async_f64(mapa(smem_u32(&ptag[qb * R + k]), peer), __longlong_as_double(bd.r0 + k), pbar);
+                        }
+                    const unsigned ctx = 8u * (unsigned)nbd;
+#else
+                    const unsigned ctx = 0u;
+#endif
                     // the peer group's W stores per row (+ on CTA 0 the peer's "inputs read" token per row)
-                    if (wig == 0) mb4_expect_tx(&bar_dot[qb], (BIC_F4_EXP & 8) ? 0u : 8u * (unsigned)nbd * (W + (h == 0 ? 1 : 0)));
+                    if (wig == 0) mb4_expect_tx(&bar_dot[qb], (BIC_F4_EXP & 8) ? 0u : 8u * (unsigned)nbd * (W + (h == 0 ? 1 : 0)) + ctx);
                     else mb4_arrive_local(&bar_dot[qb]);
                     if (warp == 0) F4_T(id, 2);
                 }
@@ -494,6 +527,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                 double qq[R];
 #pragma unroll
                 for (int k = 0; k < R; ++k) qq[k] = k < nba ? qv[qb * R + k] : 0.0;
+#if F4_CHECK_ON
+                for (int k = 0; k < nba; ++k)
+                    if (qtag[qb * R + k] != ba.r0 + k && lane == 0) atomicAdd(&g_f4_errors, 1ull);
+#endif
                 const int sa = pa.s;
                 pa.adv(nring, GR);
                 const bool acta = a.active[nda];
@@ -577,6 +614,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
             // phase (CTA-scope acquire, as for TMA) makes them visible; no cluster-scope acquire
             mb4_wait_cta(&bar_dot[qb], (unsigned)((i / QB) & 1));
             if (lane == 0) F4_T(i, 5);
+#if F4_CHECK_ON
+            if (lane < c0.n) {
+                const int q = qb * R + lane;
+                const long long want = c0.r0 + lane;
+                if (ctag[q] != want || (!(BIC_F4_EXP & 8) && ptag[q] != want)) atomicAdd(&g_f4_errors, 1ull);
+            }
+#endif
             if (lane < c0.n) {
                 const int q = qb * R + lane;
                 double qq = 0.0;
@@ -599,6 +643,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                     qq = p + dl;
                 }
                 qv[q] = qq;
+#if F4_CHECK_ON
+                qtag[q] = c0.r0 + lane;
+#endif
             }
             if (R > 1) __syncwarp();
             if (lane == 0) {
@@ -650,6 +697,9 @@ int f4_launch_r2(int dtype, int GR, int EV, const Fused2Args& a, int loss, doubl
                  int grid, cudaStream_t s);
 int f4_launch_r4(int dtype, int GR, int EV, const Fused2Args& a, int loss, double rho, int nring, int dly, size_t smem,
                  int grid, cudaStream_t s);
+int f4_errors_r1(unsigned long long* out);
+int f4_errors_r2(unsigned long long* out);
+int f4_errors_r4(unsigned long long* out);
 int f4_trace_set_r1(void* p);
 int f4_trace_set_r2(void* p);
 int f4_trace_set_r4(void* p);

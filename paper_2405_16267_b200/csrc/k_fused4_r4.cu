@@ -28,4 +28,13 @@ int f4_trace_set_r4(void* p) {
 #endif
 }
 
+int f4_errors_r4(unsigned long long* out) {
+#ifdef BIC_F4_CHECK
+    return cudaMemcpyFromSymbol(out, g_f4_errors, sizeof(*out)) == cudaSuccess ? 0 : -6;
+#else
+    *out = 0;
+    return 0;
+#endif
+}
+
 }  // namespace bic
