@@ -119,7 +119,7 @@ typedef struct {
     int32_t refit;        /* refit on the final support: LS closed-form ridge (DESIGN R19), logistic and softmax
                              damped Newton (DESIGN R29, single rank); hinge: x_final = z on T */
     int32_t sweep;        /* inner-sweep schedule: 0 = auto (the fastest measured: the CTA-pair single-pass
-                             kernel for tall single-block nodes with C == 1 and rows >= 14 KB, else
+                             kernel for tall single-block nodes with C == 1 and rows >= 5.5 KB, else
                              two-pass; BICADMM_FIELD_SWEEP_KIND reports the choice),
                              1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),
                              2 = fused single HBM pass (needs every node's blocks on this rank and

@@ -689,16 +689,16 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             if (!ok4) { delete h; return BICADMM_ERR_INVALID; }
             kind = 4;
         } else if (R->sweep == 0) {
-            // auto: the CTA-pair single-pass sweep (k_fused4) where eligible -- measured on B200
-            // (profiles/r01_summary.md) 1.45 ms vs 2.43 ms for the two HBM passes on configs[1];
-            // kinds 1-3 are slower than the two-pass sweep, which is taken otherwise
-            // rows narrower than 14 KB leave the single-pass kernel bound by its per-row chain
-            // (Table-1 shape, 300k rows, solve time: n = 1500 FP64 520 ms fused vs 496 two-pass;
-            // n = 2000 535 vs 609; n = 3000 573 vs 878)
+            // auto: the CTA-pair single-pass sweep (k_fused4) where eligible and the rows are at
+            // least 5.5 KB; narrower rows leave it bound by its per-batch chain.  Measured on B200
+            // (round 2, row batches; 4 nodes x 60M / n rows, sweeps/s single vs two passes,
+            // tools/crossover.sh): FP64 n = 500 859 vs 971, n = 800 1,270 vs 1,201, n = 2000
+            // 2,410 vs 1,277; FP32 n = 1000 1,524 vs 1,604, n = 1400 1,882 vs 1,757, n = 3000
+            // 2,844 vs 1,888.  (Round 1, one row per batch: the crossover was 14 KB.)
             int64_t maxc = 0;
             for (auto& L : h->blk) maxc = std::max(maxc, L.nj);
             const int64_t row_bytes = maxc * (P->dtype == BICADMM_F64 ? 8 : 4);
-            kind = ok4 && row_bytes >= 14336 ? 4 : 0;
+            kind = ok4 && row_bytes >= 5632 ? 4 : 0;
         }
         h->fused_kind = kind;
         h->fused = kind != 0;

@@ -387,9 +387,9 @@ def test_fused4_widest_rows_e17(bc, loss):
 
 
 def test_auto_sweep_choice(bc):
-    # sweep = 0: the CTA-pair single-pass kernel for rows >= 14 KB (C = 1, single-block
+    # sweep = 0: the CTA-pair single-pass kernel for rows >= 5.5 KB (C = 1, single-block
     # nodes), two-pass otherwise
-    for n, want in ((1792, 4), (1788, 0)):
+    for n, want in ((704, 4), (700, 0)):
         P = dg.generate(2, 4000, n, 10, "logistic", seed=2)   # tall blocks (m_i > n_j)
         s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(kappa=10),
                        dg.block_partition(n, 1))
