@@ -462,6 +462,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_ttt and args.config == "C2":
         ttt = {"configs[1]": time_to_tol_c2(bc, dg, np, torch, args),
                "table1": time_to_tol(bc, dg, np, torch, args.sweep)}
+    if rank == 0 and world == 1 and not args.no_ttt and args.config == "C1":
+        ttt = {"configs[0]": time_to_tol_c1(bc, dg, np, torch)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "C2":
         o = oracle_sample(args.cpu_m, args.cpu_n, args.inner, max(1, args.cpu_sweeps // args.inner), 0, n, m)
@@ -536,6 +538,41 @@ def time_to_tol_c2(bc, dg, np, torch, args):
     del P
     torch.cuda.empty_cache()
     return out
+
+
+def time_to_tol_c1(bc, dg, np, torch, seeds=10):
+    """configs[0] to tolerance on the GPU and on the oracle ("C1 and C2 run the
+    full time-to-tol on the oracle"): 2 nodes x 100 x 50, kappa = 5, K_in = 10, eps = 1e-4;
+    GPU device time (CUDA events, setup + solve in a CUDA-graph while loop) against the
+    oracle's wall time on the host, same seeds, same outer-iteration count expected."""
+    from oracle import oracle as orc
+    rows = []
+    for seed in range(seeds):
+        P = dg.generate(2, 100, 50, 5, "ls", seed=seed)
+        cs = dg.block_partition(50, 1)
+        prm = dict(kappa=5, max_outer=2000, inner_fixed=10, refit=1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "ls", bc.Params(**prm), cs)
+        rep = s.solve()
+        e1.record()
+        torch.cuda.synchronize()
+        gpu_s = e0.elapsed_time(e1) / 1e3
+        sup = s.support()
+        s.close()
+        t0 = time.time()
+        ref = orc.run(orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LS, 1, np.array(cs)),
+                      orc.Params(**prm))
+        cpu_s = time.time() - t0
+        rows.append(dict(seed=seed, gpu_s=gpu_s, oracle_s=cpu_s, outer_gpu=rep.outer_iters, outer_oracle=ref["iters"],
+                         converged=bool(rep.converged), same_support=sup.tolist() == ref["support"].tolist()))
+    return {"workload": "configs[0]: sparse LS, 2 nodes x 100 x 50, kappa = 5, K_in = 10, eps = 1e-4, LS refit",
+            "seeds": seeds, "gpu_s_median": float(np.median([r["gpu_s"] for r in rows])),
+            "oracle_s_median": float(np.median([r["oracle_s"] for r in rows])),
+            "oracle_cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+            "same_outer_iterations": all(r["outer_gpu"] == r["outer_oracle"] for r in rows),
+            "same_support": all(r["same_support"] for r in rows), "runs": rows}
 
 
 def time_to_tol(bc, dg, np, torch, sweep):
