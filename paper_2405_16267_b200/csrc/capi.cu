@@ -1084,6 +1084,10 @@ static int enqueue_fixed(bicadmm_handle* h, const std::vector<int>& want, int ma
     return BICADMM_OK;
 }
 
+static bool graph_nccl_enabled() {   // BICADMM_GRAPH_NCCL=0: multi-rank runs stay eager
+    static const bool on = [] { const char* e = getenv("BICADMM_GRAPH_NCCL"); return !(e && atoi(e) == 0); }();
+    return on;
+}
 static bool graph_enabled() {   // BICADMM_GRAPH=0: eager launches (read per outer iteration)
     const char* e = getenv("BICADMM_GRAPH");
     return !(e && atoi(e) == 0);
@@ -1178,10 +1182,12 @@ extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info
                 maxs = std::max(maxs, want[li]);
                 uniform = uniform && want[li] == want[0];
             }
-            // from the second outer iteration on, a fixed uniform schedule replays one CUDA graph
-            // (single rank only: multi-rank runs keep the eager launches, NCCL outside graphs)
+            // from the second outer iteration on, a fixed uniform schedule replays one CUDA graph;
+            // with NCCL its collectives are captured into it too (NCCL supports stream capture;
+            // every rank captures the same sequence).  The emulated communicator meets at host
+            // barriers, which a graph cannot hold: eager launches there.
             const bool use_graph = graph_enabled() && !replay && uniform && k >= 1 && !h->graph.failed &&
-                                   !multi_rank(h);
+                                   !(h->comm && h->comm->emu) && (!multi_rank(h) || graph_nccl_enabled());
             static const bool gdbg = getenv("BICADMM_GRAPH_DEBUG") != nullptr;
             if (gdbg) fprintf(stderr, "bicadmm: outer %d use_graph %d (replay %d uniform %d failed %d)\n", k, (int)use_graph,
                               (int)replay, (int)uniform, (int)h->graph.failed);

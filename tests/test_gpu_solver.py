@@ -522,6 +522,46 @@ def test_nccl_one_rank_path_matches_local(bc, case, split):
     assert _rel(b["xf"], a["xf"]) <= 1e-11
 
 
+@pytest.mark.parametrize("split", ["1", "2"], ids=["world_sums", "split_block_sums"])
+def test_nccl_collectives_captured_in_the_outer_graph(bc, split, capfd):
+    # fixed inner schedule: from the second outer iteration on, one outer iteration (sweeps,
+    # the NCCL AllReduces, the global step, the scalar read-back) is replayed as a CUDA graph
+    # with the collectives captured in it; the iterates equal the local run's
+    import os
+    P = dg.generate(3, 300, 120, 8, "logistic", seed=7)
+    cs = dg.block_partition(120, 2)
+    out = {}
+    for mode in ("local", "nccl"):
+        comm = None
+        os.environ["BICADMM_GRAPH_DEBUG"] = "1"
+        if mode == "nccl":
+            os.environ["BICADMM_NCCL_SELF"] = split
+        try:
+            if mode == "nccl":
+                comm = bc.bicadmm_comm_init(1, 0, torch.cuda.current_device(), None, 0)
+            s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic",
+                           bc.Params(kappa=8, max_outer=40, inner_fixed=4, refit=0, eps_p=0, eps_d=0, eps_b=0), cs,
+                           comm=comm)
+            zs = []
+            for _ in range(6):
+                s.iterate(1)
+                zs.append(s.z)
+            out[mode] = (np.array(zs), s.trace())
+            s.close()
+        finally:
+            os.environ.pop("BICADMM_NCCL_SELF", None)
+            os.environ.pop("BICADMM_GRAPH_DEBUG", None)
+            bc.bicadmm_comm_destroy(comm)
+        err = capfd.readouterr().err
+        assert "captured outer-iteration graph" in err, (mode, err[-500:])
+    (za, ta), (zb, tb) = out["local"], out["nccl"]
+    if split == "1":
+        assert np.array_equal(za, zb) and np.array_equal(ta, tb)
+    else:
+        for k in range(6):
+            assert _rel(zb[k], za[k]) <= 1e-13, k
+
+
 @pytest.mark.parametrize("loss,C,bad", [("logistic", 1, 0.5), ("hinge", 1, 0.0), ("softmax", 3, 3.0),
                                         ("softmax", 3, 1.5), ("softmax", 3, -1.0), ("ls", 1, float("nan"))])
 def test_domain_error_from_the_c_abi(bc, loss, C, bad):
