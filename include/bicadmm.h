@@ -117,7 +117,7 @@ typedef struct {
                              and ||x_i^new - x_i^old|| <= eps_inner */
     int32_t max_inner;    /* tol mode cap */
     int32_t refit;        /* refit on the final support: LS closed-form ridge (DESIGN R19), logistic and softmax
-                             damped Newton (DESIGN R29, single rank); hinge: x_final = z on T */
+                             damped Newton (DESIGN R29; multi-rank: node sums over the ranks); hinge: x_final = z on T */
     int32_t sweep;        /* inner-sweep schedule: 0 = auto (the fastest measured: the CTA-pair single-pass
                              kernel for tall single-block nodes with C == 1 and rows >= 5.5 KB, else
                              two-pass; BICADMM_FIELD_SWEEP_KIND reports the choice),

@@ -29,6 +29,16 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// NVTX ranges around the ABI entry points (header-only NVTX v3: no-ops unless a profiler
+// injects itself, e.g. nsys; names "bicadmm_setup", "bicadmm_iterate", ...)
+#include <nvtx3/nvToolsExt.h>
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 using namespace bic;
 
 // ======================================================================= handle
@@ -640,6 +650,7 @@ static int check_placement(bicadmm_handle* h) {
 // ======================================================================= setup
 extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, bicadmm_comm* comm, void* ws,
                              size_t ws_bytes, void* stream, bicadmm_handle** out) {
+    NvtxRange nvtx_range("bicadmm_setup");
     if (!out) return BICADMM_ERR_INVALID;
     *out = nullptr;
     std::string why;
@@ -1163,6 +1174,7 @@ static int sweeps_for(bicadmm_handle* h, int k, int li) {
 }
 
 extern "C" int bicadmm_iterate(bicadmm_handle* h, int n_outer, bicadmm_step_info* info) {
+    NvtxRange nvtx_range("bicadmm_iterate");
     if (!h) return BICADMM_ERR_INVALID;
     if (h->dead) return BICADMM_ERR_STATE;
     if (n_outer < 0) return fail(h, BICADMM_ERR_INVALID, "n_outer < 0");
@@ -1254,6 +1266,10 @@ __global__ void k_scatter_support(const double* __restrict__ z, const int64_t* _
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < *cnt) xf[sup[k]] = z[sup[k]];
 }
+__global__ void k_scale(int64_t n, double a, double* __restrict__ x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] *= a;
+}
+
 __global__ void k_sum_partials(const double* __restrict__ parts, int64_t n, double* out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
@@ -1348,8 +1364,29 @@ static int do_refit_newton(bicadmm_handle* h) {
     const int64_t kp = h->rf_kp, rows = h->rf_rows, len = h->len;
     const int C = h->C;
     const bool sm = h->loss == BICADMM_SOFTMAX;
-    const double lam = h->prm.lambda;
     cudaStream_t st = h->st;
+    // Multi-rank (DESIGN R29): a node's support columns are gathered on every rank that holds
+    // some of its blocks and summed over the node group (the others are zero), so each rank
+    // of a group holds the node's whole support matrix and computes the node's terms
+    // identically; node sums (objective, gradient, Hessian) are then summed over all ranks and
+    // divided by the group size gs (a node's terms are replicated gs times; gs is a power of
+    // two in every placement built here, so the division is exact).  The ridge term enters
+    // once: lambda / G_n per rank, G_n = world / gs node groups.  The Newton decisions are then
+    // taken on identical bits on every rank.
+    const bool mr = multi_rank(h);
+    const double gs = (mr && h->split_blocks) ? (double)h->gsize : 1.0;
+    const double gn = mr ? (double)h->comm->world / gs : 1.0;
+    const double lam = h->prm.lambda;
+    const double lam_part = lam / gn;
+    auto node_sum = [&](double* buf, int64_t n) -> int {   // world sum / gs (no-op on one rank)
+        if (!mr) return BICADMM_OK;
+        H_RC(h, allreduce(h, buf, n, false));
+        if (gs != 1.0) {
+            k_scale<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1184), 256, 0, st>>>(n, 1.0 / gs, buf);
+            BIC_LAUNCHED();
+        }
+        return BICADMM_OK;
+    };
     H_CUDA(h, cudaMemsetAsync(h->rf_AT, 0, sizeof(double) * rows * kp, st));
     {
         int64_t off = 0;
@@ -1361,6 +1398,7 @@ static int do_refit_newton(bicadmm_handle* h) {
             H_RC(h, launch_to_f64(h->dtype, nd.m, nd.b, h->rf_b + off, st));
             off += nd.m;
         }
+        if (mr && h->split_blocks) H_RC(h, allreduce(h, h->rf_AT, rows * kp, true));   // the node's other blocks
     }
     int64_t cnt = 0;
     H_CUDA(h, cudaMemcpyAsync(&cnt, h->support_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -1392,6 +1430,12 @@ static int do_refit_newton(bicadmm_handle* h) {
         H_CUDA(h, cudaStreamSynchronize(st));
         double sum = 0.0, xx = 0.0;
         for (double p : parts) sum += p;
+        if (mr) {   // the data term summed over the ranks' nodes (the partial counts differ by rank)
+            H_CUDA(h, cudaMemcpyAsync(h->rf_d, &sum, sizeof(double), cudaMemcpyHostToDevice, st));
+            H_RC(h, node_sum(h->rf_d, 1));
+            H_CUDA(h, cudaMemcpyAsync(&sum, h->rf_d, sizeof(double), cudaMemcpyDeviceToHost, st));
+            H_CUDA(h, cudaStreamSynchronize(st));
+        }
         for (int64_t a = 0; a < kp; ++a) xx += v[a] * v[a];
         f = sum + 0.5 * lam * xx;
         return BICADMM_OK;
@@ -1408,15 +1452,19 @@ static int do_refit_newton(bicadmm_handle* h) {
             gt.p = h->rf_G; gt.r = h->rf_Y;
             H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, C));   // Y = AT^T (P - E_y)
             H_RC(h, launch_rf_sm_scale(rows, kp, C, h->rf_AT, h->rf_P, h->support, h->support_count, h->rf_BT, h->rf_U, st));
-            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam_part, h->rf_F, ldf, false, st));
             H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_U, kp, 1.0, 0.0, h->rf_F2, ldf, false, st));
             H_RC(h, launch_rf_sm_combine(kp, ldf, C, h->support, h->support_count, h->rf_F, h->rf_F2, st));
+            H_RC(h, node_sum(h->rf_Y, kp * C));
+            H_RC(h, node_sum(h->rf_F, ldf * kp));
         } else {
             H_RC(h, launch_rf_logit(rows, h->rf_b, h->rf_w, h->rf_psi, h->rf_sd, h->rf_obj, st));
             gt.p = h->rf_psi; gt.r = h->rf_g;
             H_RC(h, launch_gemv_t(BICADMM_F64, &gt, 1, 1.0, 0.0, st, nullptr, 1));    // AT^T psi
             H_RC(h, launch_rf_scale_rows(rows, kp, h->rf_AT, h->rf_sd, h->rf_BT, st));
-            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam, h->rf_F, ldf, false, st));
+            H_RC(h, launch_gram(BICADMM_F64, rows, kp, h->rf_BT, kp, 1.0, lam_part, h->rf_F, ldf, false, st));
+            H_RC(h, node_sum(h->rf_g, kp));
+            H_RC(h, node_sum(h->rf_F, ldf * kp));
         }
         // (padding columns >= |T| are zero in AT: their Hessian rows are lambda I, step 0)
         int rc = factor_inverse(kp, h->rf_F, ldf, h->rf_H, kp, BICADMM_F64, h->rf_ws, st);
@@ -1472,9 +1520,8 @@ static int do_finalize(bicadmm_handle* h) {
     k_scatter_support<<<(unsigned)((kk + 255) / 256), 256, 0, h->st>>>(h->z, h->support, h->support_count, h->x_final);
     BIC_LAUNCHED();
     if (h->prm.refit && h->loss == BICADMM_LS) H_RC(h, do_refit(h));
-    // logistic / softmax refit (DESIGN R29): single rank (the gathered support matrix is local)
-    if (h->prm.refit && (h->loss == BICADMM_LOGISTIC || h->loss == BICADMM_SOFTMAX) && h->rf_AT &&
-        !multi_rank(h))
+    // logistic / softmax refit (DESIGN R29), single- or multi-rank
+    if (h->prm.refit && (h->loss == BICADMM_LOGISTIC || h->loss == BICADMM_SOFTMAX) && h->rf_AT)
         H_RC(h, do_refit_newton(h));
     // data term per node from p = sum_j A_ij x_final_j
     std::vector<GemvDesc> ax;
@@ -1532,6 +1579,7 @@ static void fill_report(bicadmm_handle* h, bicadmm_report* rep) {
 }
 
 extern "C" int bicadmm_finalize(bicadmm_handle* h, bicadmm_report* rep) {
+    NvtxRange nvtx_range("bicadmm_finalize");
     if (!h) return BICADMM_ERR_INVALID;
     if (h->dead) return BICADMM_ERR_STATE;
     int rc = do_finalize(h);
@@ -1656,6 +1704,7 @@ static int solve_device_loop(bicadmm_handle* h) {
 }
 
 extern "C" int bicadmm_solve(bicadmm_handle* h, bicadmm_report* rep) {
+    NvtxRange nvtx_range("bicadmm_solve");
     if (!h) return BICADMM_ERR_INVALID;
     if (h->dead) return BICADMM_ERR_STATE;
     H_CUDA(h, cudaEventRecord(h->e0, h->st));

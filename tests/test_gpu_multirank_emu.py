@@ -215,3 +215,31 @@ def test_emulated_bad_placement_fails_on_every_rank(bc):
     with pytest.raises(bc.BicadmmError) as e:
         run_emulated(bc, P, cs, "ls", prm, 2, "block", 1, plans=plans)
     assert e.value.rc == bc.ERR_PLACEMENT
+
+
+NEWTON_REFIT_CASES = [
+    # name, N, m_i, n, kappa, loss, M, C, G, mode
+    ("logistic_blockmajor_G2", 2, 400, 96, 8, "logistic", 2, 1, 2, "block"),
+    ("logistic_blockmajor_G4", 2, 400, 96, 8, "logistic", 4, 1, 4, "block"),
+    ("logistic_nodemajor_G2", 2, 400, 96, 8, "logistic", 1, 1, 2, "node"),
+    ("logistic_grid_2x2", 2, 400, 96, 8, "logistic", 2, 1, 4, "auto"),
+    ("softmax_blockmajor_G2", 1, 500, 48, 12, "softmax", 2, 3, 2, "block"),
+]
+
+
+@pytest.mark.parametrize("case", NEWTON_REFIT_CASES, ids=[c[0] for c in NEWTON_REFIT_CASES])
+def test_emulated_newton_refit(bc, orc, case):
+    # logistic / softmax damped-Newton refit on the support (DESIGN R29) across ranks: support
+    # columns summed over the node group, node sums (objective, gradient, Hessian) over all
+    # ranks; every rank takes the same Newton steps and reaches the oracle's refit
+    _, N, m, n, kappa, loss, M, C, G, mode = case
+    P = dg.generate(N, m, n, kappa, loss, seed=53, C=C)
+    cs = dg.block_partition(n, M)
+    prm = dict(kappa=kappa, max_outer=15, inner_fixed=4, refit=1, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    out = run_emulated(bc, P, cs, loss, prm, G, mode, 15)
+    ref = oracle_run(orc, P, cs, loss, prm)
+    for o in out:
+        assert o["sup"].tolist() == ref["support"].tolist()
+        assert np.array_equal(o["xf"], out[0]["xf"])
+        assert _rel(o["xf"], ref["x_final"]) <= 1e-9, _rel(o["xf"], ref["x_final"])
+        assert abs(o["obj"] - ref["objective"]) <= 1e-9 * abs(ref["objective"])
