@@ -167,13 +167,15 @@ def test_ls_refit_matches_oracle(bc, orc, M):
     assert abs(rep.objective - ref["objective"]) <= 1e-9 * abs(ref["objective"])
 
 
-@pytest.mark.parametrize("sweep", [1, 2], ids=["two_pass", "fused"])
-def test_tol_mode_inner_loop_and_replay(bc, orc, sweep):
+@pytest.mark.parametrize("sweep,n,m", [(1, 120, 300), (2, 120, 300), (2, 4000, 4100)],
+                         ids=["two_pass", "fused", "fused_n4000_batches_of_2"])
+def test_tol_mode_inner_loop_and_replay(bc, orc, sweep, n, m):
     # DESIGN R7 / S:382: tolerance-mode inner loop on the GPU; its per-(outer, node)
     # counts replayed by the oracle reproduce the GPU iterates to 1e-9, and agree
-    # with the oracle's own tolerance-mode counts (boundary flips are allowed but rare)
-    P = dg.generate(3, 300, 120, 6, "logistic", seed=21)
-    cs = dg.block_partition(120, 2 if sweep == 1 else 1)   # the single-pass sweep: one block per node
+    # with the oracle's own tolerance-mode counts (boundary flips are allowed but rare).
+    # n = 4000: the single pass with row batches of 2 and 3 row groups, nodes dropping out
+    P = dg.generate(3, m, n, 6, "logistic", seed=21)
+    cs = dg.block_partition(n, 2 if sweep == 1 else 1)   # the single-pass sweep: one block per node
     K = 8
     prm = dict(kappa=6, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=60, refit=0,
                eps_p=0.0, eps_d=0.0, eps_b=0.0)
