@@ -48,6 +48,13 @@ __device__ __forceinline__ double ld_h(const float* p) {
     asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return (double)v;
 }
+// raw element loads (FP32 tiles keep 16 floats, not 16 doubles, while the loads are in flight)
+__device__ __forceinline__ double ld_raw(const double* p) { return ld_h(p); }
+__device__ __forceinline__ float ld_raw(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
 
 // one reduce-scatter step over lane bit O: 2*HALF values -> HALF values
 template <int HALF, int O>
@@ -62,7 +69,7 @@ __device__ __forceinline__ void rs_step(double* a, int lane) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSymvThreads) k_symv_tiles(const SymvBatch B) {
+__global__ void __launch_bounds__(kSymvThreads, sizeof(T) == 4 ? 6 : 1) k_symv_tiles(const SymvBatch B) {
     __shared__ double xi[kTS], xj[kTS];
     __shared__ double colp[4][kTS];
     __shared__ double rowp[2][kTS];
@@ -77,9 +84,9 @@ __global__ void __launch_bounds__(kSymvThreads) k_symv_tiles(const SymvBatch B) 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = w >> 1, hc = w & 1;
     const int c = hc * 32 + lane;
     const T* tile = static_cast<const T*>(D.H) + t * (int64_t)(kTS * kTS) + (g * 16) * kTS + c;
-    double v[16];
+    T vr[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = ld_h(tile + i * kTS);
+    for (int i = 0; i < 16; ++i) vr[i] = ld_raw(tile + i * kTS);
     if (tid < kTS) {
         const int64_t r = I * kTS + tid;
         xi[tid] = r < D.n ? D.x[r] : 0.0;
@@ -91,13 +98,14 @@ __global__ void __launch_bounds__(kSymvThreads) k_symv_tiles(const SymvBatch B) 
     // column dots (T^T x_I)[c] over this thread's 16 rows, rows ascending
     double cs = 0.0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cs = fma(v[i], xi[g * 16 + i], cs);
+    for (int i = 0; i < 16; ++i) cs = fma((double)vr[i], xi[g * 16 + i], cs);
     colp[g][c] = cs;
     if (!diag) {
         // row dots (T x_J)[row] over this warp's 32 columns: lane reduce-scatter
         const double xc = xj[c];
+        double v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] *= xc;
+        for (int i = 0; i < 16; ++i) v[i] = (double)vr[i] * xc;
         rs_step<8, 16>(v, lane);
         rs_step<4, 8>(v, lane);
         rs_step<2, 4>(v, lane);
