@@ -312,7 +312,12 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         solver.iterate(1)
-    solver.set_profiling(not args.no_prof)
+    # per-phase CUDA events inside the timed region (the roofline's live kernel times) cost
+    # ~1 % at configs[1]; at the launch-bound configs[0] they also disable the CUDA-graph replay
+    # (3.3x), so there the timed region runs without them and a second, profiled pass of the
+    # same K steps supplies the kernel table
+    prof_in_timed = not args.no_prof and args.config != "C1"
+    solver.set_profiling(prof_in_timed)
     launches0 = solver.launches()
     clocks = ClockSampler(local)
     if world > 1:
@@ -330,6 +335,11 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     launches = solver.launches() - launches0
+    if not prof_in_timed and not args.no_prof:   # the separate profiled pass (configs[0])
+        solver.set_profiling(True)
+        for _ in range(args.steps):
+            solver.iterate(1)
+        torch.cuda.synchronize()
     phases = solver.phases()
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -497,6 +507,8 @@ def run_ours(args):
             "roofline": None if dom is None else {
                 "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
+                "timing": "CUDA events inside the timed region" if prof_in_timed else
+                          "CUDA events of a second, profiled pass of the same K steps (launch-bound config)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
             "kernels": kernels,
             "cpu_baseline": cpu,
