@@ -151,7 +151,9 @@ struct bicadmm_handle {
     int refit_iters = 0;
     // single-pass sweep (k_fused4.cu): CTA-pair clusters over static row ranges
     bool fused = false;
-    int fused_kind = 0;            // 0 two-pass, 4 single pass (k_fused4); BICADMM_FIELD_SWEEP_KIND
+    int fused_kind = 0;            // 0 two-pass, 4 single pass (k_fused4), 5 small nodes in one CTA
+                                   // (k_small_sweeps); BICADMM_FIELD_SWEEP_KIND
+    std::vector<SmallNode> small;  // kind 5: one descriptor per node
     std::vector<GemvTDesc> gtf;
     Fused2Args f2{};
     int f2grid = 0;
@@ -648,6 +650,34 @@ static int check_placement(bicadmm_handle* h) {
 }
 
 // ======================================================================= setup
+// Small nodes (kind 5, auto schedule only): single rank, C == 1, every block tall and local, a
+// node's blocks and factors fit one CTA's shared memory.  configs[0] (2 x 100 x 50): the whole
+// inner loop is one launch instead of ~6 per sweep (the path is launch-bound there).
+static bool build_small(bicadmm_handle* h) {
+    static const bool on = [] { const char* e = getenv("BICADMM_SMALL"); return !(e && atoi(e) == 0); }();
+    if (!on || h->comm || h->C != 1 || h->loss == BICADMM_SOFTMAX || h->split_blocks) return false;
+    std::vector<SmallNode> v(h->nod.size());
+    for (size_t li = 0; li < h->nod.size(); ++li) {
+        const LNode& nd = h->nod[li];
+        SmallNode& N = v[li];
+        N = SmallNode{};
+        N.b = nd.b; N.nu = nd.nu; N.delta = nd.delta; N.omega = nd.obar; N.m = nd.m;
+        for (auto& L : h->blk) {
+            if (L.li != (int)li) continue;
+            if (L.fat || N.nb >= kSmallMaxBlocks) return false;
+            SmallBlock& B = N.blk[N.nb++];
+            B.A = L.A; B.lda = L.lda; B.nj = L.nj; B.c0 = L.c0; B.cs = N.ncols;
+            B.H = L.H; B.ldh = L.ldh; B.hpack = L.hpack ? 1 : 0;
+            B.x = L.x; B.r = L.r; B.p = L.p; B.u = L.u;
+            N.ncols += L.nj;
+        }
+        small_sweep_plan(N);
+        if (N.nb != h->M || small_sweep_smem_bytes(N) > kSmallSmemMax) return false;
+    }
+    h->small = v;
+    return true;
+}
+
 extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, bicadmm_comm* comm, void* ws,
                              size_t ws_bytes, void* stream, bicadmm_handle** out) {
     NvtxRange nvtx_range("bicadmm_setup");
@@ -711,8 +741,9 @@ extern "C" int bicadmm_setup(const bicadmm_problem* P, const bicadmm_params* R, 
             const int64_t row_bytes = maxc * (P->dtype == BICADMM_F64 ? 8 : 4);
             kind = ok4 && row_bytes >= 5632 ? 4 : 0;
         }
+        if (kind == 0 && R->sweep == 0 && build_small(h)) kind = 5;
         h->fused_kind = kind;
-        h->fused = kind != 0;
+        h->fused = kind == 4;
         if (kind == 4 && build_fused4(h) != BICADMM_OK) { delete h; return BICADMM_ERR_CUDA; }
     }
     if (cudaMallocHost(&h->host_sc, sizeof(OuterScalars)) != cudaSuccess ||
@@ -1086,6 +1117,21 @@ static int enqueue_fixed(bicadmm_handle* h, const std::vector<int>& want, int ma
     std::vector<int> swept;
     for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > 0) swept.push_back((int)li);
     if (h->any_fat) H_RC(h, fat_prepare(h, swept));
+    if (!h->small.empty() && maxs > 0 && (int)swept.size() == (int)h->nod.size() &&
+        std::all_of(want.begin(), want.end(), [&](int w) { return w == maxs; })) {
+        // every node the same K sweeps: the whole inner loop in one launch (kind 5)
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        const int64_t l0 = g_launches.load();
+        if (h->prof) { e0 = next_event(h); rec_event(h, e0); }
+        H_RC(h, launch_small_sweeps(h->loss, h->dtype, h->small.data(), (int)h->small.size(), h->z, maxs, h->M,
+                                    h->prm.rho_l, h->prm.rho_c, h->st));
+        if (h->prof) {
+            e1 = next_event(h);
+            rec_event(h, e1);
+            h->pending.push_back({7, e0, e1, g_launches.load() - l0});
+        }
+        return BICADMM_OK;
+    }
     for (int sw = 0; sw < maxs; ++sw) {
         std::vector<int> active;
         for (size_t li = 0; li < h->nod.size(); ++li) if (want[li] > sw) active.push_back((int)li);

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include <cfloat>
+#include <algorithm>
 
 namespace bic {
 
@@ -278,6 +279,220 @@ int launch_psum(int C, ProxNode* nodes, int nn, double* const* /*S_out*/, cudaSt
         }
         if (t == 0) continue;
         k_psum<<<(unsigned)t, 256, 0, s>>>(B, nullptr, C);
+        BIC_LAUNCHED();
+    }
+    return BICADMM_OK;
+}
+
+}  // namespace bic
+
+namespace bic {
+
+// ----------------------------------------------------------------------------- small nodes
+// Whole inner loops of small nodes in one CTA each (configs[0]-sized problems are launch-
+// bound: ~70 graph launches per outer iteration, 3 us each).  The node's blocks A_ij and
+// their factors H_ij are staged into shared memory once; then K sweeps of Eqs. (22)-(24),
+// each: q_j = p_j + delta; r_j = rho_l A_j^T q_j + rho_c (z_j - u_j); x_j = H_j r_j;
+// p_j = A_j x_j; per sample S = sum_j p_j, abar = S / M, omega = prox(abar + nu) (22),
+// nu += abar - omega (23), delta = omega - abar - nu -- the same algebra, state and prox
+// functions as the two-pass sweep, every sum sequential in a fixed order.
+constexpr int kSmallBatchNodes = 24;   // nodes per launch (kernel parameter space: 32 KB)
+struct SmallSweepBatch {
+    SmallNode n[kSmallBatchNodes];
+    int nn;
+};
+
+__device__ __forceinline__ double small_h(const SmallBlock& B, int64_t r, int64_t c, bool f64) {
+    if (B.hpack) {   // lower 64 x 64 tiles, tile (I, J), I >= J, at I(I+1)/2 + J (k_symv.cu)
+        if (r < c) { const int64_t t = r; r = c; c = t; }
+        const int64_t I = r >> 6, J = c >> 6, e = (I * (I + 1) / 2 + J) * 4096 + (r & 63) * 64 + (c & 63);
+        return f64 ? static_cast<const double*>(B.H)[e] : (double)static_cast<const float*>(B.H)[e];
+    }
+    const int64_t e = r * B.ldh + c;
+    return f64 ? static_cast<const double*>(B.H)[e] : (double)static_cast<const float*>(B.H)[e];
+}
+
+template <typename T, int LOSS>
+__global__ void __launch_bounds__(256) k_small_sweeps(const __grid_constant__ SmallSweepBatch SB, const double* z, int K,
+                                                      int M, double rho_l, double rho_c) {
+    extern __shared__ double sm[];
+    const SmallNode& N = SB.n[blockIdx.x];
+    const int64_t m = N.m, n = N.ncols;
+    const int nb = N.nb;
+    // shared layout: A (m x n, blocks side by side), H_j (n_j x n_j each), z - u (n), r (n),
+    // x (n), p (nb x m), nu, delta, omega, b (m)
+    double* As = sm;
+    double* Hs = As + m * n;
+    int64_t hoff[kSmallMaxBlocks];
+    int64_t hsz = 0;
+    for (int j = 0; j < nb; ++j) { hoff[j] = hsz; hsz += N.blk[j].nj * N.blk[j].nj; }
+    double* zu = Hs + hsz;
+    double* rs = zu + n;
+    double* xs = rs + n;
+    double* ps = xs + n;
+    double* nus = ps + nb * m;
+    double* dls = nus + m;
+    double* oms = dls + m;
+    double* bs = oms + m;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const bool f64 = sizeof(T) == 8;
+    for (int j = 0; j < nb; ++j) {
+        const SmallBlock& B = N.blk[j];
+        const T* A = static_cast<const T*>(B.A);
+        for (int64_t e = tid; e < m * B.nj; e += nt) {
+            const int64_t r = e / B.nj, l = e % B.nj;
+            As[r * n + B.cs + l] = (double)A[r * B.lda + l];
+        }
+        for (int64_t e = tid; e < B.nj * B.nj; e += nt) Hs[hoff[j] + e] = small_h(B, e / B.nj, e % B.nj, f64);
+        for (int64_t l = tid; l < B.nj; l += nt) {
+            zu[B.cs + l] = z[B.c0 + l] - B.u[l];
+            xs[B.cs + l] = B.x[l];
+        }
+        for (int64_t r = tid; r < m; r += nt) ps[j * m + r] = B.p[r];
+    }
+    for (int64_t r = tid; r < m; r += nt) {
+        nus[r] = N.nu[r];
+        dls[r] = N.delta[r];
+        oms[r] = N.omega ? N.omega[r] : 0.0;
+        bs[r] = (double)static_cast<const T*>(N.b)[r];
+    }
+    __syncthreads();
+    const double Md = (double)M;
+    // every product splits its inner length over S = nt / outputs threads (partials in a
+    // [S][outputs] scratch, then summed by the output's thread in ascending split order)
+    double* part = bs + m;   // scratch: max(n, m) * ns doubles (small_sweep_smem_bytes)
+    const int ns = N.nsplit;
+    for (int s = 0; s < K; ++s) {
+        // r = rho_l A^T (p + delta) + rho_c (z - u): outputs = columns, inner = rows
+        for (int64_t e = tid; e < n * ns; e += nt) {
+            const int64_t l = e % n, sp = e / n;
+            int j = 0;
+            while (j + 1 < nb && l >= N.blk[j + 1].cs) ++j;
+            const int64_t r0 = m * sp / ns, r1 = m * (sp + 1) / ns;
+            double acc = 0.0;
+            for (int64_t r = r0; r < r1; ++r) acc = fma(As[r * n + l], ps[j * m + r] + dls[r], acc);
+            part[sp * n + l] = acc;
+        }
+        __syncthreads();
+        for (int64_t l = tid; l < n; l += nt) {
+            double acc = 0.0;
+            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + l];
+            rs[l] = rho_l * acc + rho_c * zu[l];
+        }
+        __syncthreads();
+        // x_j = H_j r_j: outputs = the block's rows, inner = its columns
+        for (int64_t e = tid; e < n * ns; e += nt) {
+            const int64_t l = e % n, sp = e / n;
+            int j = 0;
+            while (j + 1 < nb && l >= N.blk[j + 1].cs) ++j;
+            const SmallBlock& B = N.blk[j];
+            const double* H = Hs + hoff[j] + (l - B.cs) * B.nj;
+            const int64_t c0 = B.nj * sp / ns, c1 = B.nj * (sp + 1) / ns;
+            double acc = 0.0;
+            for (int64_t c = c0; c < c1; ++c) acc = fma(H[c], rs[B.cs + c], acc);
+            part[sp * n + l] = acc;
+        }
+        __syncthreads();
+        for (int64_t l = tid; l < n; l += nt) {
+            double acc = 0.0;
+            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + l];
+            xs[l] = acc;
+        }
+        __syncthreads();
+        // p_j = A_j x_j: outputs = (block, row), inner = the block's columns
+        const int nsm = N.nsplit_m;
+        for (int64_t e = tid; e < (int64_t)nb * m * nsm; e += nt) {
+            const int64_t o = e % (nb * m), sp = e / (nb * m);
+            const int j = (int)(o / m);
+            const int64_t r = o % m;
+            const SmallBlock& B = N.blk[j];
+            const int64_t c0 = B.nj * sp / nsm, c1 = B.nj * (sp + 1) / nsm;
+            double acc = 0.0;
+            for (int64_t c = c0; c < c1; ++c) acc = fma(As[r * n + B.cs + c], xs[B.cs + c], acc);
+            part[sp * nb * m + o] = acc;
+        }
+        __syncthreads();
+        // block sums and the per-sample prox (22)-(23): one thread per row
+        for (int64_t r = tid; r < m; r += nt) {
+            double S = 0.0;
+            for (int j = 0; j < nb; ++j) {
+                double acc = 0.0;
+                for (int sp = 0; sp < nsm; ++sp) acc += part[sp * nb * m + j * m + r];
+                ps[j * m + r] = acc;
+                S += acc;
+            }
+            const double abar = S / Md, pa = abar + nus[r];
+            double om;
+            if constexpr (LOSS == BICADMM_LS) om = (2.0 * bs[r] + rho_l * pa) / (2.0 * Md + rho_l);
+            else if constexpr (LOSS == BICADMM_LOGISTIC) om = prox_logistic(M, rho_l, bs[r], pa, N.omega ? oms[r] : pa);
+            else om = prox_hinge(M, rho_l, bs[r], pa);
+            const double nu = nus[r] + abar - om;
+            nus[r] = nu;
+            dls[r] = om - abar - nu;
+            oms[r] = om;
+        }
+        __syncthreads();
+    }
+    for (int j = 0; j < nb; ++j) {
+        const SmallBlock& B = N.blk[j];
+        for (int64_t l = tid; l < B.nj; l += nt) {
+            B.x[l] = xs[B.cs + l];
+            B.r[l] = rs[B.cs + l];
+        }
+        for (int64_t r = tid; r < m; r += nt) B.p[r] = ps[j * m + r];
+    }
+    for (int64_t r = tid; r < m; r += nt) {
+        N.nu[r] = nus[r];
+        N.delta[r] = dls[r];
+        if (N.omega) N.omega[r] = oms[r];
+    }
+}
+
+size_t small_sweep_smem_bytes(const SmallNode& N) {
+    int64_t hsz = 0;
+    for (int j = 0; j < N.nb; ++j) hsz += N.blk[j].nj * N.blk[j].nj;
+    const int64_t scratch = std::max<int64_t>(N.ncols * N.nsplit, (int64_t)N.nb * N.m * N.nsplit_m);
+    return sizeof(double) * (size_t)(N.m * N.ncols + hsz + 3 * N.ncols + N.nb * N.m + 4 * N.m + scratch);
+}
+// splits of the inner length per output (256 threads per CTA)
+void small_sweep_plan(SmallNode& N) {
+    N.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / std::max<int64_t>(1, N.ncols)));
+    N.nsplit_m = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / std::max<int64_t>(1, (int64_t)N.nb * N.m)));
+}
+
+int launch_small_sweeps(int loss, int dtype, const SmallNode* nodes, int nn, const double* z, int K, int M,
+                        double rho_l, double rho_c, cudaStream_t s) {
+    if (loss == BICADMM_SOFTMAX) return BICADMM_ERR_INVALID;
+    for (int base = 0; base < nn; base += kSmallBatchNodes) {
+        SmallSweepBatch B;
+        B.nn = nn - base < kSmallBatchNodes ? nn - base : kSmallBatchNodes;
+        size_t smem = 0;
+        for (int k = 0; k < B.nn; ++k) {
+            B.n[k] = nodes[base + k];
+            smem = smem > small_sweep_smem_bytes(B.n[k]) ? smem : small_sweep_smem_bytes(B.n[k]);
+        }
+        if (smem > kSmallSmemMax) return BICADMM_ERR_INVALID;
+#define BIC_SMALL(T, L)                                                                                      \
+    {                                                                                                        \
+        static bool set = false;                                                                             \
+        if (!set) {                                                                                          \
+            if (cudaFuncSetAttribute(k_small_sweeps<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                     (int)kSmallSmemMax) != cudaSuccess)                                     \
+                return BICADMM_ERR_CUDA;                                                                     \
+            set = true;                                                                                      \
+        }                                                                                                    \
+        k_small_sweeps<T, L><<<B.nn, 256, smem, s>>>(B, z, K, M, rho_l, rho_c);                              \
+    }
+        if (dtype == BICADMM_F64) {
+            if (loss == BICADMM_LS) BIC_SMALL(double, BICADMM_LS)
+            else if (loss == BICADMM_LOGISTIC) BIC_SMALL(double, BICADMM_LOGISTIC)
+            else BIC_SMALL(double, BICADMM_HINGE)
+        } else {
+            if (loss == BICADMM_LS) BIC_SMALL(float, BICADMM_LS)
+            else if (loss == BICADMM_LOGISTIC) BIC_SMALL(float, BICADMM_LOGISTIC)
+            else BIC_SMALL(float, BICADMM_HINGE)
+        }
+#undef BIC_SMALL
         BIC_LAUNCHED();
     }
     return BICADMM_OK;

@@ -78,6 +78,34 @@ struct ProxNode {
     int64_t cta_begin;    // filled by the launcher
 };
 int launch_prox(int loss, int dtype, int C, int M, double rho_l, ProxNode* nodes, int nn, cudaStream_t s);
+
+// Small nodes (k_prox.cu): K whole sweeps of a node in one CTA, A_ij and H_ij staged in shared
+// memory (C == 1, tall blocks, every block of the node local).
+constexpr int kSmallMaxBlocks = 8;
+constexpr size_t kSmallSmemMax = 220 * 1024;
+struct SmallBlock {
+    const void* A;       // A_ij (dtype), row stride lda
+    int64_t lda, nj;
+    int64_t c0;          // first column of the block in the n-vector (z)
+    int64_t cs;          // first column of the block in the node's staged matrix
+    const void* H;       // H_ij (dtype): packed lower 64 x 64 tiles (hpack) or nj x ldh
+    int64_t ldh;
+    int hpack;
+    double *x, *r, *p;   // x_ij, r_ij (nj), p_ij (m)
+    const double* u;     // u_ij (nj)
+};
+struct SmallNode {
+    const void* b;
+    double *nu, *delta, *omega;
+    int64_t m, ncols;
+    int nb;
+    int nsplit, nsplit_m;   // inner-length splits of the column / row products (small_sweep_plan)
+    SmallBlock blk[kSmallMaxBlocks];
+};
+void small_sweep_plan(SmallNode& N);
+size_t small_sweep_smem_bytes(const SmallNode& N);
+int launch_small_sweeps(int loss, int dtype, const SmallNode* nodes, int nn, const double* z, int K, int M,
+                        double rho_l, double rho_c, cudaStream_t s);
 int launch_psum(int C, ProxNode* nodes, int nn, double* const* S_out, cudaStream_t s);
 constexpr int kProxThreads = 256;
 // Per-CTA partials of sum_r phi((sum_j p_j)[r], b_r) for the objective (DESIGN R20).

@@ -542,8 +542,8 @@ def test_nccl_collectives_captured_in_the_outer_graph(bc, split, capfd):
             if mode == "nccl":
                 comm = bc.bicadmm_comm_init(1, 0, torch.cuda.current_device(), None, 0)
             s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic",
-                           bc.Params(kappa=8, max_outer=40, inner_fixed=4, refit=0, eps_p=0, eps_d=0, eps_b=0), cs,
-                           comm=comm)
+                           bc.Params(kappa=8, max_outer=40, inner_fixed=4, refit=0, eps_p=0, eps_d=0, eps_b=0, sweep=1),
+                           cs, comm=comm)   # the same two-pass kernels on both sides (small nodes would take kind 5 locally)
             zs = []
             for _ in range(6):
                 s.iterate(1)
@@ -596,3 +596,28 @@ def test_domain_error_from_the_c_abi(bc, loss, C, bad):
         else:
             assert rc == bc.ERR_DOMAIN
             assert not h.value
+
+
+SMALL_CASES = [
+    # name, N, m_i, n, kappa, loss, M, K, K_in, dtype
+    ("c1_ls", 2, 100, 50, 5, "ls", 1, 30, 10, "f64"),
+    ("logistic_blocks2", 3, 200, 96, 6, "logistic", 2, 12, 5, "f64"),
+    ("hinge_blocks3", 2, 150, 90, 6, "hinge", 3, 12, 4, "f64"),
+    ("logistic_fp32", 2, 180, 64, 5, "logistic", 1, 12, 5, "f32"),
+]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
+def test_small_nodes_whole_inner_loop_in_one_cta(bc, orc, case):
+    # sweep kind 5 (auto, single rank, C == 1, nodes that fit one CTA's shared memory): the K
+    # sweeps of an outer iteration in one launch; iterates against the oracle
+    _, N, m, n, kappa, loss, M, K, K_in, dt = case
+    dtype = torch.float64 if dt == "f64" else torch.float32
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, dtype=dtype, sweep=0)
+    assert solver.sweep_kind() == (5, 0)
+    tol = 1e-9 if dt == "f64" else 1e-4
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= tol, (k, _rel(zs[k], ref["z_trace"][k]))
+        assert _rel(xs[k], ref["x_trace"][k].ravel()) <= tol, k
+    assert solver.support().tolist() == ref["support"].tolist()
+    assert abs(rep.objective - ref["objective"]) <= tol * abs(ref["objective"])
