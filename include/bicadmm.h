@@ -119,7 +119,9 @@ typedef struct {
     int32_t refit;        /* refit on the final support: LS closed-form ridge (DESIGN R19), logistic and softmax
                              damped Newton (DESIGN R29; multi-rank: node sums over the ranks); hinge: x_final = z on T */
     int32_t sweep;        /* inner-sweep schedule: 0 = auto (the fastest measured: the CTA-pair single-pass
-                             kernel for tall single-block nodes with C == 1 and rows >= 5.5 KB, else
+                             kernel for tall single-block nodes with C == 1 and rows >= 5.5 KB; else, on a
+                             single rank with C == 1 and nodes whose blocks and factors fit one CTA's
+                             shared memory, whole inner loops in one CTA per node (kind 5); else
                              two-pass; BICADMM_FIELD_SWEEP_KIND reports the choice),
                              1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),
                              2 = fused single HBM pass (needs every node's blocks on this rank and
@@ -165,8 +167,8 @@ typedef enum {
                                     profiling is on (CUDA events on the handle's stream) */
     BICADMM_FIELD_PHASE_COUNT = 13, /* int64 [BICADMM_NPHASE]: kernel launches per phase while profiling */
     BICADMM_FIELD_SWEEP_KIND = 14, /* int32 [2]: inner-sweep implementation chosen at setup (0 two-pass,
-                                     4 the CTA-pair single-pass kernel k_fused4) and the number of local
-                                     Woodbury (fat) blocks */
+                                     4 the CTA-pair single-pass kernel k_fused4, 5 small nodes' inner
+                                     loops in one CTA each) and the number of local Woodbury (fat) blocks */
     BICADMM_FIELD_P_LOCAL = 15,  /* per local block in blocks[] order: p_ij = A_ij x_ij of the last sweep
                                     (m_i*C each, concatenated; property checks at full size) */
     BICADMM_FIELD_R_LOCAL = 16   /* per local block: r_ij = rho_l A_ij^T q + rho_c (z_j - u_ij) of the last
