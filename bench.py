@@ -81,6 +81,8 @@ def parse():
     if a.placement is None:
         a.placement = pr.get("placement", "node")
     a.workload = pr["workload"]
+    if a.dtype == "f32":   # the presets name the paper's FP64 arithmetic; say what this run stores
+        a.workload = a.workload.replace("FP64", "FP32 storage")
     if a.config == "C3w":   # weak scaling W3: one 12,500-column block per GPU
         G = int(os.environ.get("WORLD_SIZE", a.gpus))
         a.n, a.M, a.kappa = 12_500 * G, G, 125 * G

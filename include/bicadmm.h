@@ -124,8 +124,9 @@ typedef struct {
                              shared memory, whole inner loops in one CTA per node (kind 5); else
                              two-pass; BICADMM_FIELD_SWEEP_KIND reports the choice),
                              1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),
-                             2 = fused single HBM pass (needs every node's blocks on this rank and
-                             C == 1, else BICADMM_ERR_INVALID).  Same algebra (Eqs. (22)-(24));
+                             2 = fused single HBM pass (needs every node's blocks on this rank,
+                             C == 1, tall blocks of an even width and 16-byte row pitches, else
+                             BICADMM_ERR_INVALID).  Same algebra (Eqs. (22)-(24));
                              results agree to rounding. */
 } bicadmm_params;
 

@@ -524,7 +524,9 @@ static bool fused4_eligible(bicadmm_handle* h) {
     for (auto& nd : h->nod) if (nd.np != 1) return false;
     const int64_t es = h->dtype == BICADMM_F64 ? 8 : 4;
     for (auto& L : h->blk)
-        if (L.fat || L.nj > fused4_max_cols(h->dtype) || L.nj < 8 || (L.nj * es) % 16 || (L.lda * es) % 16) return false;
+        // whole 2-element vectors per half-row; rows 16-byte aligned (a half-row whose bytes are
+        // not a 16-byte multiple is copied rounded up into the row's own padding, inside lda)
+        if (L.fat || L.nj > fused4_max_cols(h->dtype) || L.nj < 8 || (L.nj & 1) || (L.lda * es) % 16) return false;
     return true;
 }
 

@@ -115,10 +115,10 @@ int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid
     const F4Plan p = f4_plan(dtype, a.max_cols_pad);
     if (p.EV < 0) return BICADMM_ERR_INVALID;
     const size_t es = dtype == BICADMM_F64 ? 8 : 4;
-    // TMA bulk copies: both half-rows start 16-byte aligned (ch % 4 == 0, lda * size % 16 == 0)
-    // and are whole 16-byte multiples
+    // TMA bulk copies: both half-rows start 16-byte aligned (ch % 4 == 0, lda * size % 16 == 0);
+    // a half-row of an odd number of float pairs is copied rounded up to 16 bytes, inside lda
     for (int k = 0; k < a.nn; ++k)
-        if ((a.ncols[k] * (int64_t)es) % 16 || (a.lda[k] * (int64_t)es) % 16) return BICADMM_ERR_INVALID;
+        if ((a.ncols[k] & 1) || (a.lda[k] * (int64_t)es) % 16) return BICADMM_ERR_INVALID;
     const size_t half_el = (size_t)(((a.max_cols_pad / 2 + 3) / 4) * 4 + 4);   // the kernel's half_pad
     const size_t smem = (size_t)p.nring * p.R * half_el * es;
     if (smem > (size_t)kF4RingBytes) return BICADMM_ERR_INVALID;

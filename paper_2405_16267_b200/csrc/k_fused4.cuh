@@ -344,8 +344,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
         while (k + 1 < a.nn && r >= a.row_off[k + 1]) ++k;
         return k;
     };
-    // column split of node nd (ncols * sizeof(T) % 16 == 0): half 0 = [0, ch), half 1 = [ch, ncols), ch % 4 == 0,
-    // so both halves start 16-byte aligned and are whole 16-byte multiples (TMA bulk copy)
+    // column split of node nd (ncols even, lda * sizeof(T) % 16 == 0): half 0 = [0, ch), half 1 = [ch, ncols),
+    // ch % 4 == 0, so both halves start 16-byte aligned and hold whole 2-element vectors (TMA bulk copy)
     auto half_range = [&](int nd, int64_t& c0, int64_t& cn) {
         const int64_t nc = a.ncols[nd];
         const int64_t ch = ((nc / 2 + 3) / 4) * 4;
@@ -383,7 +383,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kF4Threads, 1)
                 if (i >= nring) mb4_wait_cta(&bar_empty[s], pw.ph ^ 1u);   // (w-1)-th release
                 int64_t c0, cn;
                 half_range(b.nd, c0, cn);
-                const unsigned bytes = (unsigned)(cn * (int64_t)sizeof(T));
+                // rounded up to a 16-byte multiple (FP32 half-rows of an odd number of pairs): the extra
+                // elements are the row's own padding inside lda, never read by the main warps
+                const unsigned bytes = (unsigned)(((cn * (int64_t)sizeof(T)) + 15) / 16 * 16);
                 mb4_expect_tx(&bar_full[s], bytes * (unsigned)b.n);
                 F4_T(i, 0);
                 if (bytes)

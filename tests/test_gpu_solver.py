@@ -364,6 +364,36 @@ def test_fused4_ragged_width(bc, orc):
     assert solver.support().tolist() == ref["support"].tolist()
 
 
+@pytest.mark.parametrize("n", [702, 1502])
+def test_fused4_fp32_half_row_rounded_copy(bc, orc, n):
+    # FP32 n_j = 2 (mod 4) (as the C5 shard width 6,250): row pitch lda = n_j + 2 (16-byte rows),
+    # the second half-row (an odd number of float pairs) is copied rounded up to 16 bytes
+    # into the row padding, which holds NaN here: a read of it would poison every iterate
+    N, m, K = 3, n + 300, 5   # tall blocks (the single pass takes m_i >= n_j)
+    P = dg.generate(N, m, n, 9, "hinge", seed=31)
+    cs = dg.block_partition(n, 1)
+    prm = dict(kappa=9, max_outer=K, inner_fixed=4, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    blocks = []
+    for k in range(N):
+        t = torch.full((m, n + 2), float("nan"), dtype=torch.float32, device="cuda")
+        t[:, :n] = P.A[k].to("cuda", torch.float32)
+        blocks.append((k, 0, t[:, :n]))
+    b = [x.to("cuda", torch.float32) for x in P.b]
+    s = bc.BiCADMM(None, b, "hinge", bc.Params(sweep=2, **prm), cs, blocks=blocks)
+    assert s.sweep_kind() == (4, 0)
+    zs = []
+    for _ in range(K):
+        s.iterate(1)
+        zs.append(s.z)
+    ref = orc.run(orc.Problem([a.float().double().numpy() for a in P.A], [x.float().double().numpy() for x in P.b],
+                              orc.HINGE, 1, np.array(cs)), orc.Params(**prm), trace_z=True)
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-4, k
+    s.finalize()
+    assert s.support().tolist() == ref["support"].tolist()
+    s.close()
+
+
 @pytest.mark.parametrize("loss", ["ls", "hinge"])
 def test_fused4_widest_rows_e17(bc, loss):
     # n_j = 12,500 FP64 (the C3 shard's block width: 50 KB half-rows, a 4-slot ring, 17

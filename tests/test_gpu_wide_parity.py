@@ -105,8 +105,8 @@ def _check(s, rep, zs, xs, ref, K, tol):
 @pytest.mark.parametrize("name", ["n10000_configs1", "n12500_configs2_block", "n6250_configs4_block",
                                   "n4000_table1"])
 def test_single_pass_sweep_at_bench_widths(bc, orc, name, dt):
-    if dt == "f32" and name in ("n6250_configs4_block", "n4000_table1"):
-        pytest.skip("FP32 is checked at the two widest instances")
+    if dt == "f32" and name == "n4000_table1":
+        pytest.skip("FP32 is checked at the three widest instances (6,250: FP32 rows padded to 6,252)")
     P, cs, ref = _oracle(orc, name)
     dtype = torch.float64 if dt == "f64" else torch.float32
     s, rep, zs, xs = _gpu(bc, P, cs, name, dtype)

@@ -39,8 +39,14 @@ def run(n, dt, loss, env, K=3, K_in=3):
         cs = dg.block_partition(n, 1)
         dtype = torch.float64 if dt == "f64" else torch.float32
         out = {}
+        lda = -(-n // 4) * 4   # rows padded to 16 bytes; the padding holds NaN (never read)
+        A = []
+        for a in P.A:
+            t = torch.full((a.shape[0], lda), float("nan"), dtype=dtype, device="cuda")
+            t[:, :n] = a.to("cuda", dtype)
+            A.append(t[:, :n])
         for sweep in (1, 2):
-            s = bc.BiCADMM([a.to("cuda", dtype) for a in P.A], [b.to("cuda", dtype) for b in P.b], loss,
+            s = bc.BiCADMM(A, [b.to("cuda", dtype) for b in P.b], loss,
                            bc.Params(kappa=10, max_outer=50, inner_fixed=K_in, refit=0, eps_p=0, eps_d=0, eps_b=0,
                                      sweep=sweep), cs)
             s.iterate(K)
@@ -58,7 +64,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
-    widths = [300, 1000, 2000, 4000, 10000] if a.quick else [300, 496, 1000, 2000, 4000, 6248, 10000, 12500]
+    widths = [300, 1000, 1502, 2000, 4000, 6250, 10000] if a.quick else [300, 496, 1000, 1502, 2000, 4000, 6248, 6250, 10000, 12500]
     plans = [{}, {"BICADMM_F4_R": 1}, {"BICADMM_F4_R": 2}, {"BICADMM_F4_R": 4}, {"BICADMM_F4_GROUPS": 1},
              {"BICADMM_F4_GROUPS": 2}, {"BICADMM_F4_GROUPS": 6, "BICADMM_F4_R": 2}, {"BICADMM_F4_D": 1},
              {"BICADMM_F4_D": 3}, {"BICADMM_F4_RING": 4}]
