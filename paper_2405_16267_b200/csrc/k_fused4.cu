@@ -24,14 +24,15 @@ int fused4_max_cols(int dtype) { return 2 * kF4MainT * f4_vt(dtype) * f4_evmax(d
 static size_t f4_half_elems(int64_t max_cols) { return (size_t)(((((max_cols + 3) / 4) * 4) / 2 + 3) / 4) * 4 + 4; }
 
 // axpy delay D (in the group's own batches; the ring holds about ngrp (D + 1) batches):
-// one group: D = 2 (measured best at C2 FP64, 5 slots; BICADMM_F4_D overrides) but at
+// D = 2 (measured best at C2 FP64, 5 slots; BICADMM_F4_D overrides) but, with one group, at
 // most nring - 3, so 2 slots keep loading (C3 shard, 4 slots of 50 KB: D = 1 runs at
 // 6.15 TB/s, D = 2 at 5.87).  Always ngrp * D <= nring - 2.
 static int f4_delay(int nring, int ngrp) {
     static int d = [] { const char* e = getenv("BICADMM_F4_D"); return e ? (atoi(e) < 1 ? 1 : atoi(e)) : 0; }();
-    // ngrp > 1: D = 1 (a group's next batch comes ngrp batches later, so the prox chain already
-    // has ngrp batch periods), which keeps the most slots loading
-    int v = d ? d : (ngrp == 1 ? kF4D : 1);
+    // ngrp > 1: D = 2 where the ring still keeps 2 slots loading, else 1 (C5 shard width
+    // n_j = 6,250, two groups: FP64 4.33 vs 4.44 ms, FP32 3.10 vs 3.21 ms per 25 GB sweep;
+    // tools/f4_plansweep.sh, profiles/r02_plansweep.md)
+    int v = d ? d : 2;
     if (v < 1) v = 1;
     while (v > 1 && ngrp * v > nring - 2) --v;
     if (!d && ngrp == 1 && v > nring - 3) v = nring - 3 < 1 ? 1 : nring - 3;
