@@ -311,6 +311,7 @@ def run_ours(args):
     t0 = time.time()
     solver = bc.BiCADMM(None, b_all, args.loss, prm, cs, blocks=blocks, comm=comm, C=C)
     setup_wall = time.time() - t0
+    kind = solver.sweep_kind()[0]
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         solver.iterate(1)
@@ -390,7 +391,6 @@ def run_ours(args):
         traffic = tr.get(key, {}).get(dom, {}).get("bytes_per_launch")
     except Exception:
         pass
-    fused_mode = phases["fused_sweep"][1] > 0
     total_phase = sum(v[0] for v in phases.values())
     kernels = {k: {"ms_per_call": (v[0] / calls(k, v) if v[1] else None), "launches": v[1],
                    "calls": calls(k, v), "share": v[0] / total_phase if total_phase else None,
@@ -502,8 +502,10 @@ def run_ours(args):
                        else f"block-major ({M} feature blocks over {world} GPU(s))",
                        "l2": "inputs larger than L2 (A = %.1f GB/rank)" % (A_bytes / 1e9),
                        "sweeps_per_s": sweeps / (ms / 1e3), "setup_wall_s": setup_wall,
-                       "inner_sweep": "fused single HBM pass (k_fused4: CTA-pair clusters, SURVEY 8(f)1)" if fused_mode
-                       else "two-pass (GEMV-T + H-apply + GEMV)",
+                       "inner_sweep": {4: "fused single HBM pass (k_fused4: CTA-pair clusters, SURVEY 8(f)1)",
+                                       5: "whole inner loops in one CTA per node (k_small_sweeps: A_ij, H_ij "
+                                          "staged in shared memory once per outer iteration)"}.get(
+                                           kind, "two-pass (GEMV-T + H-apply + GEMV)"),
                        "two_pass_equivalent_GBps": (2 * A_bytes + sum(c * c for r, c in shapes) * s) * sweeps
                        / (ms / 1e3) / 1e9},
             "roofline": None if dom is None else {

@@ -674,7 +674,7 @@ static bool build_small(bicadmm_handle* h) {
             N.ncols += L.nj;
         }
         small_sweep_plan(N);
-        if (N.nb != h->M || small_sweep_smem_bytes(N) > kSmallSmemMax) return false;
+        if (N.nb != h->M || N.ncols > kSmallMaxCols || small_sweep_smem_bytes(N) > kSmallSmemMax) return false;
     }
     h->small = v;
     return true;

@@ -20,13 +20,18 @@
 namespace bic {
 
 constexpr int kOuterThreads = 1024;
+// short vectors (configs[0]: n = 50) run the same kernels with 8 warps: the step is a chain of
+// block barriers and cross-warp reductions whose cost grows with the warp count
+constexpr int kOuterThreadsSmall = 256;
+constexpr int64_t kOuterSmall = 8192;
 constexpr int kProbes = 15;  // interior probes per multisection pass (16-way)
 
 __device__ __forceinline__ uint64_t dkey(double a) { return (uint64_t)__double_as_longlong(a); }
 __device__ __forceinline__ double kdbl(uint64_t k) { return __longlong_as_double((long long)k); }
 
 // ------------------------------------------------------------------ (7b)
-__global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double rho_c, double rho_b,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_zt(int64_t len, int N, double rho_c, double rho_b,
                                                      const double* __restrict__ wsum, const double* __restrict__ s,
                                                      double* __restrict__ wbar, double* __restrict__ z,
                                                      double* __restrict__ z_prev, OuterScalars* sc) {
@@ -38,7 +43,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
     const double v = sc->v;
     const double Nd = (double)N, Nrc = Nd * rho_c;
     double psi0 = 0.0, sw = 0.0, bmax = 0.0;
-    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+    for (int64_t l = threadIdx.x; l < len; l += NT) {
         const double w = wsum[l] / Nd;
         wbar[l] = w;
         z_prev[l] = z[l];
@@ -65,7 +70,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
             // (count(lo) == count(hi), the count is monotone in tau) that set is fixed,
             // so stopping there gives bit-for-bit the same tau as narrowing to one ulp.
             int c0 = 0;
-            for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+            for (int64_t l = threadIdx.x; l < len; l += NT) {
                 const double w = wbar[l];
                 const double dl = 1.0 - s[l] * sgn(w);
                 c0 += (dl > 0.0 && w != 0.0 && fabs(w) / dl > 0.0);
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
                     acc[p] = 0.0;
                     cn[p] = 0;
                 }
-                for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+                for (int64_t l = threadIdx.x; l < len; l += NT) {
                     const double w = wbar[l];
                     const double dl = 1.0 - s[l] * sgn(w);
                     if (dl > 0.0) {
@@ -107,31 +112,37 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
                     if (lane == 0) { probe_red[wid][p] = t; probe_cnt[wid][p] = c; }
                 }
                 __syncthreads();
-                if (threadIdx.x == 0) {
-                    int best = -1;  // largest probe with f <= 0
-                    for (int p = 0; p < kProbes; ++p) {
-                        double psi = 0.0;
-                        for (int ww = 0; ww < kOuterThreads / 32; ++ww) psi += probe_red[ww][p];
-                        const double f = Nrc * tp[p] - rho_b * (psi - v);
-                        if (f <= 0.0) best = p;
+                if (wid == 0) {
+                    // lane p < kProbes sums probe p over the warps (ascending warp order, as a
+                    // serial loop would); the new bracket is [probe best, first probe above it]
+                    const int p = lane;
+                    const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
+                    double psi = 0.0;
+                    int cp = 0;
+                    if (p < kProbes)
+                        for (int ww = 0; ww < NT / 32; ++ww) {
+                            psi += probe_red[ww][p];
+                            cp += probe_cnt[ww][p];
+                        }
+                    const bool neg = p < kProbes && Nrc * kdbl(kp) - rho_b * (psi - v) <= 0.0;
+                    const unsigned bneg = __ballot_sync(0xffffffffu, neg);
+                    const int best = bneg ? 31 - __clz((int)bneg) : -1;   // largest probe with f <= 0
+                    const uint64_t nlo = best >= 0 ? (uint64_t)__shfl_sync(0xffffffffu, (long long)kp, best) : lo;
+                    const int clo = best >= 0 ? __shfl_sync(0xffffffffu, cp, best) : s_clo;
+                    const unsigned bup = __ballot_sync(0xffffffffu, p < kProbes && p > best && kp < hi && kp > nlo);
+                    const int up = bup ? __ffs((int)bup) - 1 : -1;
+                    const uint64_t nhi = up >= 0 ? (uint64_t)__shfl_sync(0xffffffffu, (long long)kp, up) : hi;
+                    const int chi = up >= 0 ? __shfl_sync(0xffffffffu, cp, up) : s_chi;
+                    if (lane == 0) {
+                        s_lo = nlo; s_hi = nhi; s_clo = clo; s_chi = chi;
+                        s_done = clo == chi;
                     }
-                    uint64_t nlo = lo, nhi = hi;
-                    int clo = s_clo, chi = s_chi;
-                    for (int p = 0; p < kProbes; ++p) {
-                        const uint64_t kp = lo + (d / 16) * (uint64_t)(p + 1) + ((d % 16) * (uint64_t)(p + 1)) / 16;
-                        int cp = 0;
-                        for (int ww = 0; ww < kOuterThreads / 32; ++ww) cp += probe_cnt[ww][p];
-                        if (p <= best) { nlo = kp; clo = cp; }
-                        else if (kp < nhi && kp > nlo) { nhi = kp; chi = cp; break; }
-                    }
-                    s_lo = nlo; s_hi = nhi; s_clo = clo; s_chi = chi;
-                    s_done = clo == chi;
                 }
                 __syncthreads();
             }
             const double tlo = kdbl(s_lo);
             double a = 0.0, b = 0.0;
-            for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+            for (int64_t l = threadIdx.x; l < len; l += NT) {
                 const double w = wbar[l];
                 const double dl = 1.0 - s[l] * sgn(w);
                 if (dl > 0.0 && w != 0.0 && fabs(w) / dl > tlo) { a += dl * fabs(w); b += dl * dl; }
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
         tau = rho_b * (Asum - v) / (Nrc + rho_b * Bsum);
     }
     double l1 = 0.0, dz2 = 0.0;
-    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+    for (int64_t l = threadIdx.x; l < len; l += NT) {
         const double w = wbar[l];
         double zl;
         if (case1) zl = w;
@@ -167,7 +178,8 @@ __global__ void __launch_bounds__(kOuterThreads) k_zt(int64_t len, int N, double
 
 int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s, double* wbar,
               double* z, double* z_prev, OuterScalars* sc, cudaStream_t st) {
-    k_zt<<<1, kOuterThreads, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
+    if (len <= kOuterSmall) k_zt<kOuterThreadsSmall><<<1, kOuterThreadsSmall, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
+    else k_zt<kOuterThreads><<<1, kOuterThreads, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }
@@ -178,6 +190,7 @@ int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum
 // that belong to T (lowest indices first).  If nonzero_only, zero keys never count.
 struct TopK { uint64_t K; int64_t take; int64_t kk; };
 
+template <int NT>
 __device__ TopK radix_topk(int64_t len, int64_t kk, const double* __restrict__ z, bool nonzero_only) {
     __shared__ int hist[256];
     __shared__ uint64_t s_prefix;
@@ -185,7 +198,7 @@ __device__ TopK radix_topk(int64_t len, int64_t kk, const double* __restrict__ z
     TopK r;
     if (nonzero_only) {
         int cnt = 0;
-        for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) cnt += z[l] != 0.0;
+        for (int64_t l = threadIdx.x; l < len; l += NT) cnt += z[l] != 0.0;
         if (threadIdx.x == 0) s_nz = 0;
         __syncthreads();
         atomicAdd(reinterpret_cast<unsigned long long*>(&s_nz), (unsigned long long)cnt);
@@ -199,23 +212,44 @@ __device__ TopK radix_topk(int64_t len, int64_t kk, const double* __restrict__ z
     uint64_t mask = 0;
     for (int pass = 0; pass < 8; ++pass) {
         const int shift = 56 - 8 * pass;
-        for (int b = threadIdx.x; b < 256; b += kOuterThreads) hist[b] = 0;
+        for (int b = threadIdx.x; b < 256; b += NT) hist[b] = 0;
         __syncthreads();
         const uint64_t prefix = s_prefix;
-        for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) {
+        for (int64_t l = threadIdx.x; l < len; l += NT) {
             const uint64_t key = dkey(fabs(z[l]));
             if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t rem = s_rem, cum = 0;
-            int sel = 0;
-            for (int b = 255; b >= 0; --b) {
-                if (cum + hist[b] >= rem) { sel = b; rem -= cum; break; }
-                cum += hist[b];
+        if (threadIdx.x < 32) {
+            // the bin holding the rem-th largest key: lane k owns bins 255 - 8k .. 248 - 8k, an
+            // inclusive scan of the lane counts from the top finds the lane, which then walks
+            // its 8 bins (the same choice as a serial walk down from bin 255)
+            const int lane = threadIdx.x;
+            const int64_t rem = s_rem;
+            int hb[8], loc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { hb[k] = hist[255 - 8 * lane - k]; loc += hb[k]; }
+            int inc = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
             }
-            s_prefix = prefix | ((uint64_t)sel << shift);
-            s_rem = rem;
+            const int exc = inc - loc;
+            const bool mine = exc < rem && rem <= inc;
+            if (mine) {
+                int64_t cum = exc;
+                int sel = 0;
+                int64_t r2 = rem;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (cum + hb[k] >= rem) { sel = 255 - 8 * lane - k; r2 = rem - cum; break; }
+                    cum += hb[k];
+                }
+                s_prefix = prefix | ((uint64_t)sel << shift);
+                s_rem = r2;
+            }
+            // (no bin reaches rem -- not reachable with kk <= len -- leaves prefix and rem as they are)
         }
         mask |= (uint64_t)255 << shift;
         __syncthreads();
@@ -228,10 +262,10 @@ __device__ TopK radix_topk(int64_t len, int64_t kk, const double* __restrict__ z
 
 // Visit elements of T in ascending index order, contiguous range per thread.
 // f(l, rank_in_T_for_this_thread_ordering) is called for members.
-template <typename F>
+template <int NT, typename F>
 __device__ void for_members(int64_t len, const double* __restrict__ z, const TopK& tk, bool nonzero_only,
                             int64_t* scan_scratch, F f) {
-    const int64_t per = (len + kOuterThreads - 1) / kOuterThreads;
+    const int64_t per = (len + NT - 1) / NT;
     const int64_t l0 = threadIdx.x * per, l1 = l0 + per < len ? l0 + per : len;
     int64_t eq = 0, mem = 0;
     for (int64_t l = l0; l < l1; ++l) {
@@ -266,24 +300,25 @@ __device__ void for_members(int64_t len, const double* __restrict__ z, const Top
     }
 }
 
-__global__ void __launch_bounds__(kOuterThreads) k_s_update(int64_t len, int64_t kappa, const double* __restrict__ z,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_s_update(int64_t len, int64_t kappa, const double* __restrict__ z,
                                                            double* __restrict__ s, OuterScalars* sc) {
     __shared__ double scratch[32];
     __shared__ int64_t scan_scratch[32];
     const double t = sc->t, v = sc->v;
     const int64_t kk = kappa < len ? kappa : len;
-    const TopK tk = radix_topk(len, kk, z, false);
-    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) s[l] = 0.0;
+    const TopK tk = radix_topk<NT>(len, kk, z, false);
+    for (int64_t l = threadIdx.x; l < len; l += NT) s[l] = 0.0;
     __syncthreads();
     double mc = 0.0;
-    for_members(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { mc += fabs(z[l]); });
+    for_members<NT>(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { mc += fabs(z[l]); });
     const double mcap = block_sum(mc, scratch);
     const double scale = mcap > 0.0 ? fmin(fmax((t - v) / mcap, -1.0), 1.0) : 0.0;
     if (mcap > 0.0)
-        for_members(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { s[l] = scale * sgn(z[l]); });
+        for_members<NT>(len, z, tk, false, scan_scratch, [&](int64_t l, int64_t) { s[l] = scale * sgn(z[l]); });
     __syncthreads();
     double zs = 0.0;
-    for (int64_t l = threadIdx.x; l < len; l += kOuterThreads) zs += z[l] * s[l];
+    for (int64_t l = threadIdx.x; l < len; l += NT) zs += z[l] * s[l];
     zs = block_sum(zs, scratch);
     if (threadIdx.x == 0) {
         const double g = zs - t;
@@ -293,23 +328,81 @@ __global__ void __launch_bounds__(kOuterThreads) k_s_update(int64_t len, int64_t
     }
 }
 
+// len <= 256 (configs[0]): one element per thread; T = the elements whose rank under
+// (|z| descending, index ascending) is below kappa -- the same set as the radix select with
+// its ties-to-lower-index rule (DESIGN R4), found with one barrier instead of 8 select passes
+constexpr int kRankThreads = 256;
+__device__ __forceinline__ bool rank_member(int64_t len, int64_t kk, const double* __restrict__ z, bool nonzero_only,
+                                            uint64_t* keys) {
+    const int l = threadIdx.x;
+    const uint64_t key = l < len ? dkey(fabs(z[l])) : 0ull;
+    keys[l] = key;
+    __syncthreads();
+    if (l >= len || kk <= 0 || (nonzero_only && key == 0)) return false;
+    int64_t rank = 0;
+    for (int k = 0; k < len; ++k) {
+        const uint64_t o = keys[k];
+        rank += o > key || (o == key && k < l);
+    }
+    return rank < kk;
+}
+
+__global__ void __launch_bounds__(kRankThreads) k_s_update_rank(int64_t len, int64_t kappa, const double* __restrict__ z,
+                                                               double* __restrict__ s, OuterScalars* sc) {
+    __shared__ double scratch[32];
+    __shared__ uint64_t keys[kRankThreads];
+    const double t = sc->t, v = sc->v;
+    const int64_t kk = kappa < len ? kappa : len;
+    const int l = threadIdx.x;
+    const bool in = rank_member(len, kk, z, false, keys);
+    const double zl = l < len ? z[l] : 0.0;
+    const double mcap = block_sum(in ? fabs(zl) : 0.0, scratch);
+    const double scale = mcap > 0.0 ? fmin(fmax((t - v) / mcap, -1.0), 1.0) : 0.0;
+    const double sl = in && mcap > 0.0 ? scale * sgn(zl) : 0.0;
+    if (l < len) s[l] = sl;
+    const double zs = block_sum(zl * sl, scratch);
+    if (threadIdx.x == 0) {
+        const double g = zs - t;
+        sc->mcap = mcap;
+        sc->g = g;
+        sc->v = v + g;
+    }
+}
+
+__global__ void __launch_bounds__(kRankThreads) k_support_rank(int64_t len, int64_t kappa, const double* __restrict__ z,
+                                                              int64_t* __restrict__ support, int64_t* count) {
+    __shared__ uint64_t keys[kRankThreads];
+    __shared__ int64_t scan_scratch[32];
+    const int64_t kk = kappa < len ? kappa : len;
+    const bool in = rank_member(len, kk, z, true, keys);
+    int64_t total;
+    const int64_t pos = block_exclusive_scan((int64_t)in, scan_scratch, &total);   // ascending index order
+    if (in) support[pos] = threadIdx.x;
+    if (threadIdx.x == 0) *count = total;
+}
+
 int launch_s_update(int64_t len, int64_t kappa, const double* z, double* s, OuterScalars* sc, cudaStream_t st) {
-    k_s_update<<<1, kOuterThreads, 0, st>>>(len, kappa, z, s, sc);
+    if (len <= kRankThreads) k_s_update_rank<<<1, kRankThreads, 0, st>>>(len, kappa, z, s, sc);
+    else if (len <= kOuterSmall) k_s_update<kOuterThreadsSmall><<<1, kOuterThreadsSmall, 0, st>>>(len, kappa, z, s, sc);
+    else k_s_update<kOuterThreads><<<1, kOuterThreads, 0, st>>>(len, kappa, z, s, sc);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }
 
-__global__ void __launch_bounds__(kOuterThreads) k_support(int64_t len, int64_t kappa, const double* __restrict__ z,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_support(int64_t len, int64_t kappa, const double* __restrict__ z,
                                                           int64_t* __restrict__ support, int64_t* count) {
     __shared__ int64_t scan_scratch[32];
     const int64_t kk = kappa < len ? kappa : len;
-    const TopK tk = radix_topk(len, kk, z, true);
-    for_members(len, z, tk, true, scan_scratch, [&](int64_t l, int64_t pos) { support[pos] = l; });
+    const TopK tk = radix_topk<NT>(len, kk, z, true);
+    for_members<NT>(len, z, tk, true, scan_scratch, [&](int64_t l, int64_t pos) { support[pos] = l; });
     if (threadIdx.x == 0) *count = tk.kk;
 }
 
 int launch_support(int64_t len, int64_t kappa, const double* z, int64_t* support, int64_t* count, cudaStream_t st) {
-    k_support<<<1, kOuterThreads, 0, st>>>(len, kappa, z, support, count);
+    if (len <= kRankThreads) k_support_rank<<<1, kRankThreads, 0, st>>>(len, kappa, z, support, count);
+    else if (len <= kOuterSmall) k_support<kOuterThreadsSmall><<<1, kOuterThreadsSmall, 0, st>>>(len, kappa, z, support, count);
+    else k_support<kOuterThreads><<<1, kOuterThreads, 0, st>>>(len, kappa, z, support, count);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }

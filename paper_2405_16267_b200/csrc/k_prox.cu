@@ -297,6 +297,7 @@ namespace bic {
 // nu += abar - omega (23), delta = omega - abar - nu -- the same algebra, state and prox
 // functions as the two-pass sweep, every sum sequential in a fixed order.
 constexpr int kSmallBatchNodes = 24;   // nodes per launch (kernel parameter space: 32 KB)
+constexpr int kSmallThreads = kSmallMaxCols;   // one CTA per node (512 and 1024 measured no faster)
 struct SmallSweepBatch {
     SmallNode n[kSmallBatchNodes];
     int nn;
@@ -313,19 +314,21 @@ __device__ __forceinline__ double small_h(const SmallBlock& B, int64_t r, int64_
 }
 
 template <typename T, int LOSS>
-__global__ void __launch_bounds__(256) k_small_sweeps(const __grid_constant__ SmallSweepBatch SB, const double* z, int K,
+__global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_constant__ SmallSweepBatch SB, const double* z, int K,
                                                       int M, double rho_l, double rho_c) {
     extern __shared__ double sm[];
     const SmallNode& N = SB.n[blockIdx.x];
-    const int64_t m = N.m, n = N.ncols;
+    // 32-bit indices: everything below lives in one CTA's shared memory (< 2^15 doubles)
+    const int m = (int)N.m, n = (int)N.ncols;
     const int nb = N.nb;
     // shared layout: A (m x n, blocks side by side), H_j (n_j x n_j each), z - u (n), r (n),
     // x (n), p (nb x m), nu, delta, omega, b (m)
     double* As = sm;
     double* Hs = As + m * n;
-    int64_t hoff[kSmallMaxBlocks];
-    int64_t hsz = 0;
-    for (int j = 0; j < nb; ++j) { hoff[j] = hsz; hsz += N.blk[j].nj * N.blk[j].nj; }
+    int hoff[kSmallMaxBlocks], bcs[kSmallMaxBlocks + 1];
+    int hsz = 0;
+    for (int j = 0; j < nb; ++j) { hoff[j] = hsz; hsz += (int)(N.blk[j].nj * N.blk[j].nj); bcs[j] = (int)N.blk[j].cs; }
+    bcs[nb] = n;
     double* zu = Hs + hsz;
     double* rs = zu + n;
     double* xs = rs + n;
@@ -336,21 +339,46 @@ __global__ void __launch_bounds__(256) k_small_sweeps(const __grid_constant__ Sm
     double* bs = oms + m;
     const int tid = threadIdx.x, nt = blockDim.x;
     const bool f64 = sizeof(T) == 8;
+    // staging: 8 independent global loads per thread in flight before their shared stores
+    // (a load -> store chain per element costs one L2/HBM latency each: ~10 us per launch)
+    constexpr int U = 8;
     for (int j = 0; j < nb; ++j) {
         const SmallBlock& B = N.blk[j];
         const T* A = static_cast<const T*>(B.A);
-        for (int64_t e = tid; e < m * B.nj; e += nt) {
-            const int64_t r = e / B.nj, l = e % B.nj;
-            As[r * n + B.cs + l] = (double)A[r * B.lda + l];
+        const int nj = (int)B.nj, cs = bcs[j];
+        for (int e0 = 0; e0 < m * nj; e0 += U * nt) {
+            double v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int e = e0 + k * nt + tid;
+                v[k] = e < m * nj ? (double)A[(int64_t)(e / nj) * B.lda + e % nj] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int e = e0 + k * nt + tid;
+                if (e < m * nj) As[(e / nj) * n + cs + e % nj] = v[k];
+            }
         }
-        for (int64_t e = tid; e < B.nj * B.nj; e += nt) Hs[hoff[j] + e] = small_h(B, e / B.nj, e % B.nj, f64);
-        for (int64_t l = tid; l < B.nj; l += nt) {
-            zu[B.cs + l] = z[B.c0 + l] - B.u[l];
-            xs[B.cs + l] = B.x[l];
+        for (int e0 = 0; e0 < nj * nj; e0 += U * nt) {
+            double v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int e = e0 + k * nt + tid;
+                v[k] = e < nj * nj ? small_h(B, e / nj, e % nj, f64) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int e = e0 + k * nt + tid;
+                if (e < nj * nj) Hs[hoff[j] + e] = v[k];
+            }
         }
-        for (int64_t r = tid; r < m; r += nt) ps[j * m + r] = B.p[r];
+        for (int l = tid; l < nj; l += nt) {
+            zu[cs + l] = z[B.c0 + l] - B.u[l];
+            xs[cs + l] = B.x[l];
+        }
+        for (int r = tid; r < m; r += nt) ps[j * m + r] = B.p[r];
     }
-    for (int64_t r = tid; r < m; r += nt) {
+    for (int r = tid; r < m; r += nt) {
         nus[r] = N.nu[r];
         dls[r] = N.delta[r];
         oms[r] = N.omega ? N.omega[r] : 0.0;
@@ -362,62 +390,85 @@ __global__ void __launch_bounds__(256) k_small_sweeps(const __grid_constant__ Sm
     // [S][outputs] scratch, then summed by the output's thread in ascending split order)
     double* part = bs + m;   // scratch: max(n, m) * ns doubles (small_sweep_smem_bytes)
     const int ns = N.nsplit;
+    const int nsm = N.nsplit_m;
+    auto block_of = [&](int l) {
+        int j = 0;
+        while (j + 1 < nb && l >= bcs[j + 1]) ++j;
+        return j;
+    };
+    // Per-thread work, fixed for all K sweeps (hoisted: the index arithmetic was ~40 % of the
+    // instructions of a sweep).  Column phases: n <= kSmallThreads (build_small), so a thread
+    // owns at most one (column, split) slice.  Row phase: the first (row, split) item here,
+    // further items (nb m nsm > kSmallThreads) computed in the loop.
+    const bool colw = tid < n * ns;
+    const int cl = colw ? tid % n : 0, csp = colw ? tid / n : 0;
+    const int cj = block_of(cl);
+    const int cr0 = m * csp / ns, cr1 = m * (csp + 1) / ns;
+    const int hnj = bcs[cj + 1] - bcs[cj];
+    const int hc0 = hnj * csp / ns, hc1 = hnj * (csp + 1) / ns;
+    const double* aT = As + cl;
+    const double* pT = ps + cj * m;
+    const double* Hrow = Hs + hoff[cj] + (cl - bcs[cj]) * hnj;
+    const double* rj = rs + bcs[cj];
+    const int nbm = nb * m;
+    struct RowItem { int o, sp, c0, c1; const double* a; const double* x; };
+    auto row_item = [&](int e) {
+        RowItem it;
+        it.o = e % nbm;
+        it.sp = e / nbm;
+        const int j = it.o / m, r = it.o % m;
+        const int nj = bcs[j + 1] - bcs[j];
+        it.c0 = nj * it.sp / nsm;
+        it.c1 = nj * (it.sp + 1) / nsm;
+        it.a = As + r * n + bcs[j];
+        it.x = xs + bcs[j];
+        return it;
+    };
+    const RowItem ri0 = row_item(tid);
     for (int s = 0; s < K; ++s) {
         // r = rho_l A^T (p + delta) + rho_c (z - u): outputs = columns, inner = rows
-        for (int64_t e = tid; e < n * ns; e += nt) {
-            const int64_t l = e % n, sp = e / n;
-            int j = 0;
-            while (j + 1 < nb && l >= N.blk[j + 1].cs) ++j;
-            const int64_t r0 = m * sp / ns, r1 = m * (sp + 1) / ns;
+        if (colw) {
             double acc = 0.0;
-            for (int64_t r = r0; r < r1; ++r) acc = fma(As[r * n + l], ps[j * m + r] + dls[r], acc);
-            part[sp * n + l] = acc;
+#pragma unroll 4
+            for (int r = cr0; r < cr1; ++r) acc = fma(aT[r * n], pT[r] + dls[r], acc);
+            part[csp * n + cl] = acc;
         }
         __syncthreads();
-        for (int64_t l = tid; l < n; l += nt) {
+        if (tid < n) {
             double acc = 0.0;
-            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + l];
-            rs[l] = rho_l * acc + rho_c * zu[l];
+            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + tid];
+            rs[tid] = rho_l * acc + rho_c * zu[tid];
         }
         __syncthreads();
         // x_j = H_j r_j: outputs = the block's rows, inner = its columns
-        for (int64_t e = tid; e < n * ns; e += nt) {
-            const int64_t l = e % n, sp = e / n;
-            int j = 0;
-            while (j + 1 < nb && l >= N.blk[j + 1].cs) ++j;
-            const SmallBlock& B = N.blk[j];
-            const double* H = Hs + hoff[j] + (l - B.cs) * B.nj;
-            const int64_t c0 = B.nj * sp / ns, c1 = B.nj * (sp + 1) / ns;
+        if (colw) {
             double acc = 0.0;
-            for (int64_t c = c0; c < c1; ++c) acc = fma(H[c], rs[B.cs + c], acc);
-            part[sp * n + l] = acc;
+#pragma unroll 4
+            for (int c = hc0; c < hc1; ++c) acc = fma(Hrow[c], rj[c], acc);
+            part[csp * n + cl] = acc;
         }
         __syncthreads();
-        for (int64_t l = tid; l < n; l += nt) {
+        if (tid < n) {
             double acc = 0.0;
-            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + l];
-            xs[l] = acc;
+            for (int sp = 0; sp < ns; ++sp) acc += part[sp * n + tid];
+            xs[tid] = acc;
         }
         __syncthreads();
         // p_j = A_j x_j: outputs = (block, row), inner = the block's columns
-        const int nsm = N.nsplit_m;
-        for (int64_t e = tid; e < (int64_t)nb * m * nsm; e += nt) {
-            const int64_t o = e % (nb * m), sp = e / (nb * m);
-            const int j = (int)(o / m);
-            const int64_t r = o % m;
-            const SmallBlock& B = N.blk[j];
-            const int64_t c0 = B.nj * sp / nsm, c1 = B.nj * (sp + 1) / nsm;
+        for (int e = tid; e < nbm * nsm; e += nt) {
+            const RowItem it = e == tid ? ri0 : row_item(e);
             double acc = 0.0;
-            for (int64_t c = c0; c < c1; ++c) acc = fma(As[r * n + B.cs + c], xs[B.cs + c], acc);
-            part[sp * nb * m + o] = acc;
+#pragma unroll 4
+            for (int c = it.c0; c < it.c1; ++c) acc = fma(it.a[c], it.x[c], acc);
+            part[it.sp * nbm + it.o] = acc;
         }
         __syncthreads();
         // block sums and the per-sample prox (22)-(23): one thread per row
-        for (int64_t r = tid; r < m; r += nt) {
+        for (int r = tid; r < m; r += nt) {
             double S = 0.0;
             for (int j = 0; j < nb; ++j) {
                 double acc = 0.0;
-                for (int sp = 0; sp < nsm; ++sp) acc += part[sp * nb * m + j * m + r];
+                for (int sp = 0; sp < nsm; ++sp) acc += part[sp * nbm + j * m + r];
                 ps[j * m + r] = acc;
                 S += acc;
             }
@@ -435,13 +486,14 @@ __global__ void __launch_bounds__(256) k_small_sweeps(const __grid_constant__ Sm
     }
     for (int j = 0; j < nb; ++j) {
         const SmallBlock& B = N.blk[j];
-        for (int64_t l = tid; l < B.nj; l += nt) {
-            B.x[l] = xs[B.cs + l];
-            B.r[l] = rs[B.cs + l];
+        const int nj = (int)B.nj, cs = bcs[j];
+        for (int l = tid; l < nj; l += nt) {
+            B.x[l] = xs[cs + l];
+            B.r[l] = rs[cs + l];
         }
-        for (int64_t r = tid; r < m; r += nt) B.p[r] = ps[j * m + r];
+        for (int r = tid; r < m; r += nt) B.p[r] = ps[j * m + r];
     }
-    for (int64_t r = tid; r < m; r += nt) {
+    for (int r = tid; r < m; r += nt) {
         N.nu[r] = nus[r];
         N.delta[r] = dls[r];
         if (N.omega) N.omega[r] = oms[r];
@@ -454,10 +506,10 @@ size_t small_sweep_smem_bytes(const SmallNode& N) {
     const int64_t scratch = std::max<int64_t>(N.ncols * N.nsplit, (int64_t)N.nb * N.m * N.nsplit_m);
     return sizeof(double) * (size_t)(N.m * N.ncols + hsz + 3 * N.ncols + N.nb * N.m + 4 * N.m + scratch);
 }
-// splits of the inner length per output (256 threads per CTA)
+// splits of the inner length per output (kSmallThreads threads per CTA)
 void small_sweep_plan(SmallNode& N) {
-    N.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / std::max<int64_t>(1, N.ncols)));
-    N.nsplit_m = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / std::max<int64_t>(1, (int64_t)N.nb * N.m)));
+    N.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(16, kSmallThreads / std::max<int64_t>(1, N.ncols)));
+    N.nsplit_m = (int)std::max<int64_t>(1, std::min<int64_t>(16, kSmallThreads / std::max<int64_t>(1, (int64_t)N.nb * N.m)));
 }
 
 int launch_small_sweeps(int loss, int dtype, const SmallNode* nodes, int nn, const double* z, int K, int M,
@@ -481,7 +533,7 @@ int launch_small_sweeps(int loss, int dtype, const SmallNode* nodes, int nn, con
                 return BICADMM_ERR_CUDA;                                                                     \
             set = true;                                                                                      \
         }                                                                                                    \
-        k_small_sweeps<T, L><<<B.nn, 256, smem, s>>>(B, z, K, M, rho_l, rho_c);                              \
+        k_small_sweeps<T, L><<<B.nn, kSmallThreads, smem, s>>>(B, z, K, M, rho_l, rho_c);                              \
     }
         if (dtype == BICADMM_F64) {
             if (loss == BICADMM_LS) BIC_SMALL(double, BICADMM_LS)

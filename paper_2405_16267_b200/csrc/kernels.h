@@ -82,6 +82,7 @@ int launch_prox(int loss, int dtype, int C, int M, double rho_l, ProxNode* nodes
 // Small nodes (k_prox.cu): K whole sweeps of a node in one CTA, A_ij and H_ij staged in shared
 // memory (C == 1, tall blocks, every block of the node local).
 constexpr int kSmallMaxBlocks = 8;
+constexpr int kSmallMaxCols = 256;   // threads of k_small_sweeps: a node's columns fit one pass of them
 constexpr size_t kSmallSmemMax = 220 * 1024;
 struct SmallBlock {
     const void* A;       // A_ij (dtype), row stride lda
