@@ -100,6 +100,15 @@ extern "C" int bicadmm_debug_f4_trace(void* dev_buf) {   // trace builds only (B
     return r1 ? r1 : r2 ? r2 : r4;
 }
 
+// 1 in a protocol-check build (tools/build_f4_variant.sh f4check -DBIC_F4_CHECK), 0 in the product
+extern "C" int bicadmm_debug_f4_check_build(void) {
+#ifdef BIC_F4_CHECK
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 // check builds only (BIC_F4_CHECK): tag mismatches seen so far (0 in product builds)
 extern "C" unsigned long long bicadmm_debug_f4_errors(void) {
     unsigned long long a = 0, b = 0, c = 0;

@@ -27,6 +27,7 @@ def test_single_pass_protocol_tags():
     summary = [l for l in lines if "summary" in l]
     assert summary, r.stdout[-2000:] + r.stderr[-2000:]
     s = summary[0]["summary"]
+    assert s["check_build"]   # bicadmm_debug_f4_check_build() == 1: the tags were really counted
     assert s["tag_errors"] == 0, [l for l in lines if l.get("tag_errors")]
     assert s["worst_rel_f64"] <= 1e-9, s
     assert s["fused_runs"] >= 0.8 * s["runs"], s

@@ -70,6 +70,9 @@ def main():
              {"BICADMM_F4_D": 3}, {"BICADMM_F4_RING": 4}]
     if a.quick:
         plans = plans[:4] + plans[6:7]
+    if not bc.lib().bicadmm_debug_f4_check_build():   # a product build counts nothing
+        print(json.dumps({"error": "not a BIC_F4_CHECK build: set BICADMM_LIB_PATH to build_ab/f4check.so"}))
+        return 2
     rows, worst, total0 = [], 0.0, errors()
     for n, dt, plan in itertools.product(widths, ("f64", "f32"), plans):
         loss = "logistic" if n % 3 else "hinge"
@@ -81,7 +84,7 @@ def main():
         if dt == "f64":
             worst = max(worst, rel)
         print(json.dumps(rows[-1]), flush=True)
-    summary = {"runs": len(rows), "tag_errors": errors() - total0, "worst_rel_f64": worst,
+    summary = {"runs": len(rows), "check_build": True, "tag_errors": errors() - total0, "worst_rel_f64": worst,
                "fused_runs": sum(1 for r in rows if r["kind"][0] == 4)}
     print(json.dumps({"summary": summary}))
     return 0 if summary["tag_errors"] == 0 and worst <= 1e-9 else 1
