@@ -1047,17 +1047,27 @@ static int outer_step(bicadmm_handle* h, bool readback = true) {
     cudaEvent_t oa = nullptr, ob = nullptr;
     const int64_t lo0 = g_launches.load();
     if (h->prof) { oa = next_event(h); rec_event(h, oa); }
-    H_RC(h, launch_wsum(h->len, h->lenp, h->x_all, h->u_all, (int)h->nod.size(), h->wsum, h->st));
-    H_RC(h, allreduce(h, h->wsum, h->len, false));
-    H_RC(h, launch_zt(h->len, h->N, h->prm.rho_c, rho_b, h->wsum, h->s, h->wbar, h->z, h->z_prev, h->sc, h->st));
+    const double sqrtN_rho_c = std::sqrt((double)h->N) * h->prm.rho_c;
+    // single rank, short vectors: Collect runs inside k_zt and the residuals inside k_node_sq
+    // (same arithmetic, same order; two launches fewer per outer iteration)
+    const bool fuse = !multi_rank(h) && h->len * (int64_t)h->nod.size() <= (int64_t)1 << 16;
+    WsumIn cw;
+    if (fuse) {
+        cw.x_all = h->x_all; cw.u_all = h->u_all; cw.stride = h->lenp; cw.nl = (int)h->nod.size();
+    } else {
+        H_RC(h, launch_wsum(h->len, h->lenp, h->x_all, h->u_all, (int)h->nod.size(), h->wsum, h->st));
+        H_RC(h, allreduce(h, h->wsum, h->len, false));
+    }
+    H_RC(h, launch_zt(h->len, h->N, h->prm.rho_c, rho_b, h->wsum, h->s, h->wbar, h->z, h->z_prev, h->sc, h->st, cw));
     H_RC(h, launch_s_update(h->len, h->prm.kappa, h->z, h->s, h->sc, h->st));
     H_RC(h, launch_u_update(h->bv.data(), (int)h->bv.size(), h->z, h->upart, h->st));
-    H_RC(h, launch_node_sq(h->bv.data(), (int)h->bv.size(), h->upart, h->N, h->node_sq, h->st));
+    H_RC(h, launch_node_sq(h->bv.data(), (int)h->bv.size(), h->upart, h->N, h->node_sq, h->st,
+                           multi_rank(h) ? nullptr : h->sc, sqrtN_rho_c));
     if (multi_rank(h)) {
         // every (i, j) contributes exactly once: node_sq partials are per local block
         H_RC(h, allreduce(h, h->node_sq, h->N, false));
+        H_RC(h, launch_residuals(h->N, sqrtN_rho_c, h->node_sq, h->sc, h->st));
     }
-    H_RC(h, launch_residuals(h->N, std::sqrt((double)h->N) * h->prm.rho_c, h->node_sq, h->sc, h->st));
     if (h->prof) {
         ob = next_event(h);
         rec_event(h, ob);

@@ -32,9 +32,9 @@ __device__ __forceinline__ double kdbl(uint64_t k) { return __longlong_as_double
 // ------------------------------------------------------------------ (7b)
 template <int NT>
 __global__ void __launch_bounds__(NT) k_zt(int64_t len, int N, double rho_c, double rho_b,
-                                                     const double* __restrict__ wsum, const double* __restrict__ s,
+                                                     double* __restrict__ wsum, const double* __restrict__ s,
                                                      double* __restrict__ wbar, double* __restrict__ z,
-                                                     double* __restrict__ z_prev, OuterScalars* sc) {
+                                                     double* __restrict__ z_prev, OuterScalars* sc, WsumIn cw) {
     __shared__ double scratch[32];
     __shared__ double probe_red[32][kProbes + 1];
     __shared__ int probe_cnt[32][kProbes + 1];
@@ -44,7 +44,15 @@ __global__ void __launch_bounds__(NT) k_zt(int64_t len, int N, double rho_c, dou
     const double Nd = (double)N, Nrc = Nd * rho_c;
     double psi0 = 0.0, sw = 0.0, bmax = 0.0;
     for (int64_t l = threadIdx.x; l < len; l += NT) {
-        const double w = wsum[l] / Nd;
+        double ws;
+        if (cw.x_all) {   // Collect fused in (single rank, short vectors): k_wsum's sum, same order
+            ws = 0.0;
+            for (int i = 0; i < cw.nl; ++i) ws += cw.x_all[(int64_t)i * cw.stride + l] + cw.u_all[(int64_t)i * cw.stride + l];
+            wsum[l] = ws;
+        } else {
+            ws = wsum[l];
+        }
+        const double w = ws / Nd;
         wbar[l] = w;
         z_prev[l] = z[l];
         const double d = 1.0 - s[l] * sgn(w);
@@ -176,10 +184,10 @@ __global__ void __launch_bounds__(NT) k_zt(int64_t len, int N, double rho_c, dou
     }
 }
 
-int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s, double* wbar,
-              double* z, double* z_prev, OuterScalars* sc, cudaStream_t st) {
-    if (len <= kOuterSmall) k_zt<kOuterThreadsSmall><<<1, kOuterThreadsSmall, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
-    else k_zt<kOuterThreads><<<1, kOuterThreads, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc);
+int launch_zt(int64_t len, int N, double rho_c, double rho_b, double* wsum, const double* s, double* wbar,
+              double* z, double* z_prev, OuterScalars* sc, cudaStream_t st, WsumIn cw) {
+    if (len <= kOuterSmall) k_zt<kOuterThreadsSmall><<<1, kOuterThreadsSmall, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc, cw);
+    else k_zt<kOuterThreads><<<1, kOuterThreads, 0, st>>>(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc, cw);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }
@@ -514,8 +522,18 @@ struct NodeSqArgs {
     int nb;
 };
 
+__device__ __forceinline__ void residuals_body(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc) {
+    double pr = 0.0;
+    for (int i = 0; i < N; ++i) pr += sqrt(node_sq[i]);
+    sc->p_r = pr;
+    sc->d_r = sqrtN_rho_c * sqrt(sc->dz2);
+    sc->b_r = fabs(sc->g);
+}
+
+// res != nullptr (single rank: no AllReduce of node_sq in between): the residuals (15) are
+// computed here too, by thread 0 after the block barrier (one launch instead of two)
 __global__ void k_node_sq(const __grid_constant__ NodeSqArgs A, const double* __restrict__ partial, int N,
-                          double* __restrict__ node_sq) {
+                          double* __restrict__ node_sq, OuterScalars* res, double sqrtN_rho_c) {
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         double acc = 0.0;
         for (int b = 0; b < A.nb; ++b)
@@ -523,9 +541,14 @@ __global__ void k_node_sq(const __grid_constant__ NodeSqArgs A, const double* __
                 for (int64_t k = 0; k < A.count[b]; ++k) acc += partial[A.begin[b] + k];
         node_sq[i] = acc;
     }
+    if (res) {
+        __syncthreads();
+        if (threadIdx.x == 0) residuals_body(N, sqrtN_rho_c, node_sq, res);
+    }
 }
 
-int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq, cudaStream_t s) {
+int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq, cudaStream_t s,
+                   OuterScalars* res, double sqrtN_rho_c) {
     if (nb > kMaxDesc * 4) return BICADMM_ERR_PLACEMENT;
     NodeSqArgs A;
     A.nb = nb;
@@ -534,18 +557,13 @@ int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, dou
         A.count[b] = (bv[b].len + kUThreads * kUPer - 1) / (kUThreads * kUPer);
         A.node[b] = bv[b].node;
     }
-    k_node_sq<<<1, 64, 0, s>>>(A, partial, N, node_sq);
+    k_node_sq<<<1, 64, 0, s>>>(A, partial, N, node_sq, res, sqrtN_rho_c);
     BIC_LAUNCHED();
     return BICADMM_OK;
 }
 
 __global__ void k_residuals(int N, double sqrtN_rho_c, const double* __restrict__ node_sq, OuterScalars* sc) {
-    if (threadIdx.x != 0) return;
-    double pr = 0.0;
-    for (int i = 0; i < N; ++i) pr += sqrt(node_sq[i]);
-    sc->p_r = pr;
-    sc->d_r = sqrtN_rho_c * sqrt(sc->dz2);
-    sc->b_r = fabs(sc->g);
+    if (threadIdx.x == 0) residuals_body(N, sqrtN_rho_c, node_sq, sc);
 }
 
 int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s) {

@@ -171,8 +171,14 @@ struct OuterScalars {   // device-resident scalars of the global step
     double t, v, tau, g, mcap, dz2, psi0, pad0;
     double p_r, d_r, b_r, pad1;
 };
-int launch_zt(int64_t len, int N, double rho_c, double rho_b, const double* wsum, const double* s,
-              double* wbar, double* z, double* z_prev, OuterScalars* sc, cudaStream_t st);
+struct WsumIn {          // Collect inputs when k_zt computes wsum itself (x_all == nullptr: it reads wsum)
+    const double* x_all = nullptr;
+    const double* u_all = nullptr;
+    int64_t stride = 0;
+    int nl = 0;
+};
+int launch_zt(int64_t len, int N, double rho_c, double rho_b, double* wsum, const double* s,
+              double* wbar, double* z, double* z_prev, OuterScalars* sc, cudaStream_t st, WsumIn cw = WsumIn{});
 int launch_s_update(int64_t len, int64_t kappa, const double* z, double* s, OuterScalars* sc,
                     cudaStream_t st);
 int launch_support(int64_t len, int64_t kappa, const double* z, int64_t* support, int64_t* count,
@@ -195,7 +201,7 @@ int launch_seg_sums(const double* const* ptr, const int64_t* count, const int32_
                     cudaStream_t s);
 // node_sq[i] = sum over local blocks of node i (blocks[] order) of partials.
 int launch_node_sq(const BlockVec* bv, int nb, const double* partial, int N, double* node_sq,
-                   cudaStream_t s);
+                   cudaStream_t s, OuterScalars* res = nullptr, double sqrtN_rho_c = 0.0);
 int launch_residuals(int N, double sqrtN_rho_c, const double* node_sq, OuterScalars* sc, cudaStream_t s);
 constexpr int kUThreads = 256;
 

@@ -127,7 +127,7 @@ extern "C" int bicadmm_op_zt(int64_t len, int N, double rho_c, double rho_b, con
     OuterScalars h{};
     h.v = v;
     BIC_CUDA(cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-    int rc = launch_zt(len, N, rho_c, rho_b, wsum, s, wbar, z, z_prev, sc, st);
+    int rc = launch_zt(len, N, rho_c, rho_b, const_cast<double*>(wsum), s, wbar, z, z_prev, sc, st);
     if (!rc) {
         BIC_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
         BIC_CUDA(cudaStreamSynchronize(st));
