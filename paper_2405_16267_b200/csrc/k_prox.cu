@@ -324,10 +324,17 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
     // shared layout: A (m x n, blocks side by side), H_j (n_j x n_j each), z - u (n), r (n),
     // x (n), p (nb x m), nu, delta, omega, b (m)
     double* As = sm;
-    double* Hs = As + m * n;
+    // row strides padded to an odd number of doubles: lanes walking rows (the A x and H r
+    // products) then hit distinct bank pairs (an even stride such as 50 is a 4-way conflict)
+    const int lda = n | 1;
+    double* Hs = As + m * lda;
     int hoff[kSmallMaxBlocks], bcs[kSmallMaxBlocks + 1];
     int hsz = 0;
-    for (int j = 0; j < nb; ++j) { hoff[j] = hsz; hsz += (int)(N.blk[j].nj * N.blk[j].nj); bcs[j] = (int)N.blk[j].cs; }
+    for (int j = 0; j < nb; ++j) {
+        hoff[j] = hsz;
+        hsz += (int)(N.blk[j].nj * (N.blk[j].nj | 1));
+        bcs[j] = (int)N.blk[j].cs;
+    }
     bcs[nb] = n;
     double* zu = Hs + hsz;
     double* rs = zu + n;
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int e = e0 + k * nt + tid;
-                if (e < m * nj) As[(e / nj) * n + cs + e % nj] = v[k];
+                if (e < m * nj) As[(e / nj) * lda + cs + e % nj] = v[k];
             }
         }
         for (int e0 = 0; e0 < nj * nj; e0 += U * nt) {
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int e = e0 + k * nt + tid;
-                if (e < nj * nj) Hs[hoff[j] + e] = v[k];
+                if (e < nj * nj) Hs[hoff[j] + (e / nj) * (nj | 1) + e % nj] = v[k];
             }
         }
         for (int l = tid; l < nj; l += nt) {
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
     const int hc0 = hnj * csp / ns, hc1 = hnj * (csp + 1) / ns;
     const double* aT = As + cl;
     const double* pT = ps + cj * m;
-    const double* Hrow = Hs + hoff[cj] + (cl - bcs[cj]) * hnj;
+    const double* Hrow = Hs + hoff[cj] + (cl - bcs[cj]) * (hnj | 1);
     const double* rj = rs + bcs[cj];
     const int nbm = nb * m;
     struct RowItem { int o, sp, c0, c1; const double* a; const double* x; };
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
         const int nj = bcs[j + 1] - bcs[j];
         it.c0 = nj * it.sp / nsm;
         it.c1 = nj * (it.sp + 1) / nsm;
-        it.a = As + r * n + bcs[j];
+        it.a = As + r * lda + bcs[j];
         it.x = xs + bcs[j];
         return it;
     };
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
         if (colw) {
             double acc = 0.0;
 #pragma unroll 4
-            for (int r = cr0; r < cr1; ++r) acc = fma(aT[r * n], pT[r] + dls[r], acc);
+            for (int r = cr0; r < cr1; ++r) acc = fma(aT[r * lda], pT[r] + dls[r], acc);
             part[csp * n + cl] = acc;
         }
         __syncthreads();
@@ -502,9 +509,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sweeps(const __grid_con
 
 size_t small_sweep_smem_bytes(const SmallNode& N) {
     int64_t hsz = 0;
-    for (int j = 0; j < N.nb; ++j) hsz += N.blk[j].nj * N.blk[j].nj;
+    for (int j = 0; j < N.nb; ++j) hsz += N.blk[j].nj * (N.blk[j].nj | 1);   // odd row strides
     const int64_t scratch = std::max<int64_t>(N.ncols * N.nsplit, (int64_t)N.nb * N.m * N.nsplit_m);
-    return sizeof(double) * (size_t)(N.m * N.ncols + hsz + 3 * N.ncols + N.nb * N.m + 4 * N.m + scratch);
+    return sizeof(double) * (size_t)(N.m * (N.ncols | 1) + hsz + 3 * N.ncols + N.nb * N.m + 4 * N.m + scratch);
 }
 // splits of the inner length per output (kSmallThreads threads per CTA)
 void small_sweep_plan(SmallNode& N) {
