@@ -554,6 +554,43 @@ def test_nccl_one_rank_path_matches_local(bc, case, split):
     assert _rel(b["xf"], a["xf"]) <= 1e-11
 
 
+def test_nccl_one_rank_single_pass_in_the_outer_graph(bc, capfd):
+    # the multi-rank node-major path with the CTA-pair single pass (what a weak-scaling
+    # configs[1] run takes on every rank): a real one-rank NCCL communicator, the fused sweep,
+    # the per-outer AllReduces captured in the replayed outer-iteration graph; the iterates
+    # equal the local run's bit for bit (a one-rank AllReduce is a copy)
+    import os
+    P = dg.generate(3, 900, 800, 8, "logistic", seed=17)   # tall single-block nodes, 6.4 KB rows
+    cs = dg.block_partition(800, 1)
+    out = {}
+    for mode in ("local", "nccl"):
+        comm = None
+        os.environ["BICADMM_GRAPH_DEBUG"] = "1"
+        if mode == "nccl":
+            os.environ["BICADMM_NCCL_SELF"] = "1"
+        try:
+            if mode == "nccl":
+                comm = bc.bicadmm_comm_init(1, 0, torch.cuda.current_device(), None, 0)
+            s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic",
+                           bc.Params(kappa=8, max_outer=40, inner_fixed=4, refit=0, eps_p=0, eps_d=0, eps_b=0),
+                           cs, comm=comm)
+            assert s.sweep_kind() == (4, 0), (mode, s.sweep_kind())
+            zs = []
+            for _ in range(6):
+                s.iterate(1)
+                zs.append(s.z)
+            out[mode] = (np.array(zs), s.trace())
+            s.close()
+        finally:
+            os.environ.pop("BICADMM_NCCL_SELF", None)
+            os.environ.pop("BICADMM_GRAPH_DEBUG", None)
+            bc.bicadmm_comm_destroy(comm)
+        err = capfd.readouterr().err
+        assert "captured outer-iteration graph" in err, (mode, err[-500:])
+    (za, ta), (zb, tb) = out["local"], out["nccl"]
+    assert np.array_equal(za, zb) and np.array_equal(ta, tb)
+
+
 @pytest.mark.parametrize("split", ["1", "2"], ids=["world_sums", "split_block_sums"])
 def test_nccl_collectives_captured_in_the_outer_graph(bc, split, capfd):
     # fixed inner schedule: from the second outer iteration on, one outer iteration (sweeps,
