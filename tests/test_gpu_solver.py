@@ -116,6 +116,28 @@ def test_fp32_mode_within_1e4(bc, orc, sweep):
     assert abs(rep.objective - ref["objective"]) <= 1e-4 * abs(ref["objective"])
 
 
+FP32_CASES = [
+    # name, N, m_i, n, kappa, loss, M, K_outer, K_in[, C]
+    ("ls_blocks3", 2, 300, 250, 12, "ls", 3, 12, 5),
+    ("hinge_blocks2", 3, 400, 201, 8, "hinge", 2, 12, 5),
+    ("softmax_c10_blocks8", 1, 1500, 200, 20, "softmax", 8, 6, 4, 10),
+    ("softmax_c3_blocks2", 2, 300, 61, 6, "softmax", 2, 8, 5, 3),
+]
+
+
+@pytest.mark.parametrize("case", FP32_CASES, ids=[c[0] for c in FP32_CASES])
+def test_fp32_other_losses_within_1e4(bc, orc, case):
+    # FP32 storage (R23) for LS, hinge and softmax (the DMMA GEMV-C / GEMV-T-C kernels read
+    # FP32 A for C > 1): iterates within 1e-4 of the oracle run on the FP32-rounded data
+    _, N, m, n, kappa, loss, M, K, K_in = case[:9]
+    C = case[9] if len(case) > 9 else 1
+    solver, rep, zs, xs, ref, _ = run_pair(bc, orc, N, m, n, kappa, loss, M, K, K_in, C=C, dtype=torch.float32)
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-4, (k, _rel(zs[k], ref["z_trace"][k]))
+    assert solver.support().tolist() == ref["support"].tolist()
+    assert abs(rep.objective - ref["objective"]) <= 1e-4 * abs(ref["objective"])
+
+
 def test_schedule_replay_matches_oracle(bc, orc):
     # DESIGN R7: per-(outer, node) inner counts replayed identically on both sides
     P = dg.generate(3, 200, 100, 6, "logistic", seed=5)
