@@ -77,3 +77,46 @@ def test_configs1_full_size(bc):
     assert np.abs(z).sum() <= sc["t"] * (1 + 1e-12) + 1e-12
     tail = np.sort(np.abs(z))[: max(0, z.size - KAPPA)].sum()
     assert tail <= sc["b_r"] * (1 + 1e-9) + 1e-12
+
+
+def test_configs3_full_size(bc):
+    # BASELINE.json configs[3] on one GPU, the bench's C4 launch configuration: softmax, C = 10,
+    # 1 node x 500,000 x 20,000 FP64 (80 GB), M = 8 feature blocks (7 x 2,512 + 2,416 columns),
+    # the DMMA GEMV-C / GEMV-T-C two-pass sweep.  After one outer iteration of K_in = 2:
+    # sampled rows of p_ij = A_ij x_ij recomputed one by one in FP64 on the host, and every
+    # block's x-update normal equations (rho_l A_ij^T A_ij + c I) x_ij = r_ij (Eq. (24), R17)
+    # checked with FP64 library mat-vecs (torch) on the device.
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120 * 2**30:
+        pytest.skip("needs ~120 GB of free device memory")
+    Nn, m, n, C, M, kappa = 1, 500_000, 20_000, 10, 8, 500
+    P = dg.generate(Nn, m, n, kappa, "softmax", C=C, seed=1000, device="cuda")
+    cs = dg.block_partition(n, M, align=16)
+    assert [cs[j + 1] - cs[j] for j in range(M)] == [2512] * 7 + [2416]
+    s = bc.BiCADMM(P.A, P.b, "softmax", bc.Params(kappa=kappa, inner_fixed=2, max_outer=10, eps_p=0.0, eps_d=0.0,
+                                                  eps_b=0.0, refit=0), cs, C=C)
+    assert s.sweep_kind() == (0, 0)
+    s.iterate(1)
+    x = s.get(bc.FIELD_X_LOCAL)
+    p = s.get(bc.FIELD_P_LOCAL)
+    r = s.get(bc.FIELD_R_LOCAL)
+    s.close()
+    A = P.A[0]
+    rng = np.random.default_rng(3)
+    rows = np.sort(rng.choice(m, 256, replace=False))
+    Ar = A[torch.from_numpy(rows).cuda()].cpu().numpy()
+    rho_l, c = 4.0, 1.0 / (100.0 * Nn) + 4.0
+    xo, po = 0, 0
+    for j in range(M):
+        nj = cs[j + 1] - cs[j]
+        Xj = x[xo:xo + nj * C].reshape(nj, C)
+        Pj = p[po:po + m * C].reshape(m, C)
+        Rj = r[xo:xo + nj * C].reshape(nj, C)
+        ref_rows = Ar[:, cs[j]:cs[j + 1]] @ Xj
+        assert np.max(np.abs(ref_rows - Pj[rows])) <= 1e-12 * max(1.0, np.max(np.abs(ref_rows))), j
+        Aj = A[:, cs[j]:cs[j + 1]]
+        Xt = torch.from_numpy(Xj).cuda()
+        F = rho_l * (Aj.T @ (Aj @ Xt)) + c * Xt
+        assert _rel(F.cpu().numpy(), Rj) <= 1e-10, j
+        xo += nj * C
+        po += m * C
