@@ -125,7 +125,8 @@ typedef struct {
                              two-pass; BICADMM_FIELD_SWEEP_KIND reports the choice),
                              1 = two-pass (A streamed by GEMV-T then by GEMV, paper-literal order),
                              2 = fused single HBM pass (needs every node's blocks on this rank,
-                             C == 1, tall blocks of an even width and 16-byte row pitches, else
+                             C == 1, tall blocks of an even width up to 13,432 (FP64) / 13,824 (FP32)
+                             columns and 16-byte row pitches, else
                              BICADMM_ERR_INVALID).  Same algebra (Eqs. (22)-(24));
                              results agree to rounding. */
 } bicadmm_params;

@@ -518,16 +518,21 @@ static void build_descs(bicadmm_handle* h) {
 }
 
 // Single-pass sweep (k_fused4.cu) eligibility: every node's blocks local and one block per
-// node, C == 1, tall blocks, 16-byte row pieces, rows up to fused4_max_cols.
+// node, C == 1, tall blocks, 16-byte row pieces, rows up to fused4_max_cols with a feasible plan.
 static bool fused4_eligible(bicadmm_handle* h) {
     if (h->split_blocks || h->C != 1 || (int)h->nod.size() > kF2MaxNodes || h->sm_count < 2) return false;
     for (auto& nd : h->nod) if (nd.np != 1) return false;
     const int64_t es = h->dtype == BICADMM_F64 ? 8 : 4;
-    for (auto& L : h->blk)
+    int64_t maxc = 0;
+    for (auto& L : h->blk) {
         // whole 2-element vectors per half-row; rows 16-byte aligned (a half-row whose bytes are
         // not a 16-byte multiple is copied rounded up into the row's own padding, inside lda)
         if (L.fat || L.nj > fused4_max_cols(h->dtype) || L.nj < 8 || (L.nj & 1) || (L.lda * es) % 16) return false;
-    return true;
+        maxc = std::max(maxc, L.nj);
+    }
+    // and a launch plan exists for the widest row: FP64 half-rows past 52.5 KB (n_j > 13,432)
+    // leave fewer than 4 ring slots
+    return fused4_plan_ok(h->dtype, maxc);
 }
 
 static int build_fused4(bicadmm_handle* h) {

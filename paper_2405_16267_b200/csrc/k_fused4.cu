@@ -63,7 +63,7 @@ static F4Plan f4_plan(int dtype, int64_t max_cols) {
     static const int envR = [] { const char* e = getenv("BICADMM_F4_R"); return e ? atoi(e) : 0; }();
     static const int envG = [] { const char* e = getenv("BICADMM_F4_GROUPS"); return e ? atoi(e) : 0; }();
     p.R = (envR == 1 || envR == 2 || envR == 4) ? envR : 4 * hb <= 42 * 1024 ? 4 : 2 * hb <= 42 * 1024 ? 2 : 1;
-    const int64_t half = (max_cols + 1) / 2 + 2;
+    const int64_t half = ((max_cols / 2 + 3) / 4) * 4;   // the kernel's ch of the widest row (the larger half)
     auto fits = [&](int g, F4Plan& q) {   // EV within the compiled set and a feasible ring
         if (f4_ev(dtype, half, g) > f4_evmax(dtype)) return false;
         int nring = (int)(kF4RingBytes / (q.R * hb));
@@ -89,6 +89,8 @@ static F4Plan f4_plan(int dtype, int64_t max_cols) {
     p.EV = -1;
     return p;
 }
+
+bool fused4_plan_ok(int dtype, int64_t max_cols) { return f4_plan(dtype, max_cols).EV > 0; }
 
 int fused4_groups(int dtype, int64_t max_cols) {
     const F4Plan p = f4_plan(dtype, max_cols);

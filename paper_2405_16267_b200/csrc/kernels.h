@@ -222,7 +222,8 @@ struct Fused2Args {
     int64_t total_rows, max_cols_pad;
 };
 int launch_fused4(int dtype, const Fused2Args& a, int loss, double rho, int grid, cudaStream_t s);
-int fused4_max_cols(int dtype);
+int fused4_max_cols(int dtype);                     // bound of the compiled vector counts
+bool fused4_plan_ok(int dtype, int64_t max_cols);  // a launch plan exists (ring of >= 4 slots, ...)
 int fused4_groups(int dtype, int64_t max_cols);   // row groups of the CTA-pair sweep (partials per group)
 
 // ---------------------------------------------------------------- finalize vectors (k_vec.cu)

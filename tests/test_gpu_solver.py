@@ -440,6 +440,37 @@ def test_fused4_widest_rows_e17(bc, loss):
     assert _rel(out[0][1], out[1][1]) <= 1e-9
 
 
+@pytest.mark.parametrize("dt,n_max", [("f64", 13_432), ("f32", 13_824)])
+def test_fused4_maximum_width_and_beyond(bc, dt, n_max):
+    # the widest single-pass rows: FP64 13,432 columns (52.5 KB half-rows, the last width with a
+    # 4-slot ring), FP32 13,824 (fused4_max_cols: 9 two-element vectors per lane); the fused
+    # sweep against the two-pass kernels; 4 columns more and setup refuses the forced single
+    # pass (BICADMM_ERR_INVALID) and the auto choice is two-pass
+    dtype = torch.float64 if dt == "f64" else torch.float32
+    P = dg.generate(1, n_max + 100, n_max, 20, "logistic", seed=19, device="cuda", dtype=dtype)
+    cs = dg.block_partition(n_max, 1)
+    prm = dict(kappa=20, max_outer=3, inner_fixed=3, eps_p=0.0, eps_d=0.0, eps_b=0.0, refit=0)
+    out = {}
+    for sweep in (2, 1):
+        s = bc.BiCADMM(P.A, P.b, "logistic", bc.Params(sweep=sweep, **prm), cs)
+        assert s.sweep_kind()[0] == (4 if sweep == 2 else 0)
+        s.iterate(3)
+        out[sweep] = (s.z, s.get(bc.FIELD_X_LOCAL))
+        s.close()
+    assert _rel(out[2][0], out[1][0]) <= 1e-9
+    assert _rel(out[2][1], out[1][1]) <= 1e-9
+    del P
+    n2 = n_max + 4
+    P2 = dg.generate(1, n2 + 8, n2, 10, "logistic", seed=19, device="cuda", dtype=dtype)
+    cs2 = dg.block_partition(n2, 1)
+    s = bc.BiCADMM(P2.A, P2.b, "logistic", bc.Params(kappa=10, inner_fixed=1), cs2)
+    assert s.sweep_kind()[0] == 0
+    s.close()
+    with pytest.raises(bc.BicadmmError) as e:
+        bc.BiCADMM(P2.A, P2.b, "logistic", bc.Params(kappa=10, inner_fixed=1, sweep=2), cs2)
+    assert e.value.rc == bc.ERR_INVALID
+
+
 def test_auto_sweep_choice(bc):
     # sweep = 0: the CTA-pair single-pass kernel for rows >= 5.5 KB (C = 1, single-block
     # nodes), two-pass otherwise

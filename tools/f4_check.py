@@ -63,8 +63,11 @@ def run(n, dt, loss, env, K=3, K_in=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--widths", default="", help="comma-separated row widths (default: the built-in list)")
     a = ap.parse_args()
-    widths = [300, 1000, 1502, 2000, 4000, 6250, 10000] if a.quick else [300, 496, 1000, 1502, 2000, 4000, 6248, 6250, 10000, 12500]
+    widths = [300, 1000, 1502, 2000, 4000, 6250, 10000] if a.quick else [300, 496, 1000, 1502, 2000, 4000, 6248, 6250, 10000, 12500, 13300]
+    if a.widths:
+        widths = [int(w) for w in a.widths.split(",")]
     plans = [{}, {"BICADMM_F4_R": 1}, {"BICADMM_F4_R": 2}, {"BICADMM_F4_R": 4}, {"BICADMM_F4_GROUPS": 1},
              {"BICADMM_F4_GROUPS": 2}, {"BICADMM_F4_GROUPS": 6, "BICADMM_F4_R": 2}, {"BICADMM_F4_D": 1},
              {"BICADMM_F4_D": 3}, {"BICADMM_F4_RING": 4}]
