@@ -119,3 +119,40 @@ def test_solve_stops_where_the_oracle_stops_on_exact_zero_residuals(bc, orc):
     assert rep.outer_iters == 1 and rep.converged == 1
     assert np.count_nonzero(s.z) == 0
     s.close()
+
+
+# Capacity boundaries of the launch batching: more nodes than one small-sweeps launch takes
+# (24), more local blocks than one descriptor batch (64), the single pass's node table (32),
+# and the largest class count (C = 16).
+BOUNDARY_CASES = [
+    # name, N, m_i, n, kappa, loss, M, K_outer, K_in, C, expected sweep kind (None: any)
+    ("small_nodes_30_two_launches", 30, 60, 20, 3, "logistic", 1, 6, 3, 1, 5),
+    ("blocks_20x4_two_desc_batches", 20, 120, 64, 6, "ls", 4, 6, 3, 1, None),
+    ("fused_32_nodes", 32, 720, 704, 8, "logistic", 1, 3, 2, 1, 4),
+    ("fused_33_nodes_falls_back", 33, 720, 704, 8, "logistic", 1, 3, 2, 1, 0),
+    ("softmax_c16", 2, 400, 40, 8, "softmax", 2, 6, 3, 16, None),
+]
+
+
+@pytest.mark.parametrize("case", BOUNDARY_CASES, ids=[c[0] for c in BOUNDARY_CASES])
+def test_capacity_boundaries_match_oracle(bc, orc, case):
+    _, N, m, n, kappa, loss, M, K, K_in, C, kind = case
+    P = dg.generate(N, m, n, kappa, loss, seed=77, C=C)
+    cs = dg.block_partition(n, M)
+    prm = dict(kappa=kappa, max_outer=K, inner_fixed=K_in, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.cuda() for a in P.A], [x.cuda() for x in P.b], loss, bc.Params(**prm), cs, C=C)
+    if kind is not None:
+        assert s.sweep_kind()[0] == kind, s.sweep_kind()
+    zs = []
+    for _ in range(K):
+        s.iterate(1)
+        zs.append(s.z)
+    s.finalize()
+    lid = {"ls": orc.LS, "logistic": orc.LOGISTIC, "hinge": orc.HINGE, "softmax": orc.SOFTMAX}[loss]
+    oprm = dict(prm, eps_p=-1.0, eps_d=-1.0, eps_b=-1.0)
+    ref = orc.run(orc.Problem([a.numpy() for a in P.A], [x.numpy() for x in P.b], lid, C, np.array(cs)),
+                  orc.Params(**oprm), trace_z=True)
+    for k in range(K):
+        assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, (k, _rel(zs[k], ref["z_trace"][k]))
+    assert s.support().tolist() == ref["support"].tolist()
+    s.close()
