@@ -131,6 +131,9 @@ BOUNDARY_CASES = [
     ("fused_32_nodes", 32, 720, 704, 8, "logistic", 1, 3, 2, 1, 4),
     ("fused_33_nodes_falls_back", 33, 720, 704, 8, "logistic", 1, 3, 2, 1, 0),
     ("softmax_c16", 2, 400, 40, 8, "softmax", 2, 6, 3, 16, None),
+    ("nine_blocks_past_small_path", 2, 200, 72, 6, "logistic", 9, 6, 3, 1, 0),
+    ("fat_at_m_eq_n_minus_1", 2, 63, 64, 5, "ls", 1, 8, 3, 1, None),
+    ("tall_at_m_eq_n", 2, 64, 64, 5, "ls", 1, 8, 3, 1, None),
 ]
 
 
