@@ -245,8 +245,8 @@ def test_emulated_newton_refit(bc, orc, case):
         assert abs(o["obj"] - ref["objective"]) <= 1e-9 * abs(ref["objective"])
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_emulated_nodemajor_single_pass(bc, orc, G):
+@pytest.mark.parametrize("G,dt", [(2, "f64"), (4, "f64"), (2, "f32")])
+def test_emulated_nodemajor_single_pass(bc, orc, G, dt):
     # node-major weak scaling (configs[1]'s multi-GPU shape): every rank holds whole nodes and
     # runs the CTA-pair single pass (rows >= 5.5 KB); Collect and the residual partials cross
     # the ranks once per outer iteration.  Against the oracle at 1e-9, bit-identical z on all ranks.
@@ -254,7 +254,8 @@ def test_emulated_nodemajor_single_pass(bc, orc, G):
     P = dg.generate(N, m, n, 9, "logistic", seed=23)
     cs = dg.block_partition(n, 1)
     prm = dict(kappa=9, max_outer=K, inner_fixed=3, refit=0, eps_p=0.0, eps_d=0.0, eps_b=0.0, sweep=2)
-    out = run_emulated(bc, P, cs, "logistic", prm, G, "node", K)
+    dtype = torch.float64 if dt == "f64" else torch.float32
+    out = run_emulated(bc, P, cs, "logistic", prm, G, "node", K, dtype=dtype)
     oprm = {k: v for k, v in prm.items() if k != "sweep"}
-    ref = oracle_run(orc, P, cs, "logistic", oprm)
-    check_against_oracle(out, ref, cs, 1, K)
+    ref = oracle_run(orc, P, cs, "logistic", oprm, dtype=dtype)
+    check_against_oracle(out, ref, cs, 1, K, tol=1e-9 if dt == "f64" else 1e-4)
