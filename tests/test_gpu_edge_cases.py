@@ -159,3 +159,29 @@ def test_capacity_boundaries_match_oracle(bc, orc, case):
         assert _rel(zs[k], ref["z_trace"][k]) <= 1e-9, (k, _rel(zs[k], ref["z_trace"][k]))
     assert s.support().tolist() == ref["support"].tolist()
     s.close()
+
+
+def test_tol_mode_on_small_nodes(bc, orc):
+    # the inner tolerance mode on a problem whose fixed schedule takes the small-nodes
+    # path (kind 5): per-node sweep counts decided on the device values, replayed by the oracle
+    P = dg.generate(3, 100, 40, 5, "logistic", seed=12)
+    cs = dg.block_partition(40, 1)
+    K = 6
+    prm = dict(kappa=5, max_outer=K, inner_fixed=0, eps_inner=1e-6, max_inner=40, refit=0,
+               eps_p=0.0, eps_d=0.0, eps_b=0.0)
+    s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic", bc.Params(**prm), cs)
+    s.iterate(K)
+    counts = s.get(bc.FIELD_INNER_COUNTS, np.int32).reshape(K, 3)
+    pb = orc.Problem([a.numpy() for a in P.A], [b.numpy() for b in P.b], orc.LOGISTIC, 1, np.array(cs))
+    oprm = dict(prm, eps_p=-1.0, eps_d=-1.0, eps_b=-1.0)
+    own = orc.run(pb, orc.Params(**oprm))
+    rep = orc.run(pb, orc.Params(**oprm), schedule=counts)
+    assert counts.min() >= 1 and counts.max() <= 40
+    assert _rel(s.z, rep["z"]) <= 1e-9
+    assert np.mean(counts == own["inner_counts"]) >= 0.8
+    s.close()
+    # the same problem with a fixed schedule runs on the small-nodes kernel
+    s = bc.BiCADMM([a.cuda() for a in P.A], [b.cuda() for b in P.b], "logistic",
+                   bc.Params(**dict(prm, inner_fixed=4)), cs)
+    assert s.sweep_kind()[0] == 5
+    s.close()
